@@ -1,0 +1,168 @@
+/*
+ * bkg.h — C ABI of the B200-native Block-CG hot path (libbkgpu.so).
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API
+ * (namespace blockkrylov, /root/reference/proj/include/blockkrylov).  Each
+ * entry point names the reference interface it replaces.  Plain pointers and
+ * sizes only: every *host* pointer argument is ordinary (pageable or pinned)
+ * host memory; the library owns all device memory.  No exceptions cross the
+ * ABI: every call returns a bkg_status and bkg_last_error() holds the
+ * message of the last failing call on the calling thread.
+ *
+ * Numerics: every context runs in one of two modes.
+ *   BKG_NUMERICS_EXACT — reproduces the reference's operation order and
+ *     rounding (unfused mul/add, row-ordered Gram/norm chains), so results are
+ *     bit-identical to the reference CPU build (-O3 -ffp-contract=off).
+ *   BKG_NUMERICS_FAST (default) — fused sm_100a kernels (FMA, deterministic
+ *     two-stage grid reductions).  Run-to-run bit-reproducible on a given
+ *     GPU/grid; differs from the reference only by summation order.
+ * There is no CPU fallback: without a CUDA device every compute call fails
+ * with BKG_CUDA.
+ */
+#ifndef BKG_H
+#define BKG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BKG_OK = 0,
+  BKG_DIMENSION = 1, /* blockkrylov::DimensionError (errors.hpp:13-16)        */
+  BKG_CONFIG = 2,    /* blockkrylov::ConfigError    (errors.hpp:19-22)        */
+  BKG_BREAKDOWN = 3, /* blockkrylov::BreakdownError (errors.hpp:31-40)        */
+  BKG_CUDA = 4,      /* device / driver failure (no reference counterpart)    */
+  BKG_NCCL = 5,      /* collective failure (multi-GPU only)                   */
+  BKG_FACTORIZATION = 6, /* blockkrylov::FactorizationError (errors.hpp:43-52) */
+  BKG_INTERNAL = 7
+} bkg_status;
+
+/* SubalgebraMode (subalgebra.hpp:19) */
+enum { BKG_HYBRID = 0, BKG_GLOBAL = 1 };
+/* PreconditionerKind (preconditioners.hpp:317) */
+enum { BKG_PRECOND_IDENTITY = 0, BKG_PRECOND_JACOBI = 1, BKG_PRECOND_ILU0 = 2 };
+enum { BKG_NUMERICS_FAST = 0, BKG_NUMERICS_EXACT = 1 };
+
+typedef struct bkg_ctx bkg_ctx;
+typedef struct bkg_matrix bkg_matrix;
+typedef struct bkg_solver bkg_solver;
+
+/* ---- context ---------------------------------------------------------- */
+const char* bkg_last_error(void);
+const char* bkg_version(void);
+int bkg_device_count(int* count);
+int bkg_ctx_create(int device, bkg_ctx** out);
+int bkg_ctx_destroy(bkg_ctx* ctx);
+int bkg_ctx_set_numerics(bkg_ctx* ctx, int numerics);
+int bkg_ctx_get_numerics(const bkg_ctx* ctx, int* numerics);
+/* The cudaStream_t every launch of ctx is queued on (for event timing). */
+int bkg_ctx_stream(const bkg_ctx* ctx, void** stream);
+/* Number of kernels this library launched on ctx so far (evidence counter). */
+int bkg_ctx_launch_count(const bkg_ctx* ctx, uint64_t* launches);
+
+/* ---- sparse operator (SparseMatrix, sparse_matrix.hpp:27-131) ----------- */
+/* Uploads a CSR matrix with the reference's size_t (uint64) offsets/columns.
+ * Structure is validated on the host (sparse_matrix.hpp:89-105); value
+ * symmetry is the host API's job (the SparseMatrix constructor).          */
+int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* row_offsets,
+                      const uint64_t* col_indices, const double* values, bkg_matrix** out);
+int bkg_matrix_destroy(bkg_matrix* m);
+int bkg_matrix_info(const bkg_matrix* m, uint64_t* n, uint64_t* nnz);
+
+/* ---- kernels (kernels.hpp) ---------------------------------------------- */
+/* BDOT   kernels.hpp:59-88.  out: block_count*p*p doubles, row-major blocks. */
+int bkg_bdot(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, const double* x,
+             const double* y, double* out, uint64_t* flops_bdot /* nullable, += */);
+/* BAXPY  kernels.hpp:94-125.  x <- x + y * embed(gamma).                     */
+int bkg_baxpy(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, double* x,
+              const double* y, const double* gamma, uint64_t* flops_baxpy);
+/* BOP    kernels.hpp:129-164.  y <- A x.                                      */
+int bkg_bop(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, const double* x, double* y,
+            uint64_t* flops_bop);
+/* BSOLVE kernels.hpp:166-240.  On BKG_BREAKDOWN *bad_block holds the first
+ * singular block (BreakdownError::block_index).                             */
+int bkg_bsolve(bkg_ctx* ctx, uint64_t k, uint64_t p, int mode, const double* gamma,
+               const double* delta, double* out, uint64_t* bad_block);
+/* column_norms  block_vector.hpp:59-70.  out: k doubles.                     */
+int bkg_column_norms(bkg_ctx* ctx, uint64_t n, uint64_t k, const double* x, double* out);
+/* Preconditioner::apply  preconditioners.hpp:73-129 (identity / Jacobi /
+ * ILU(0) factored on device from `a`; ilu0_factor preconditioners.hpp:153-196). */
+int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k,
+                      const double* r, double* z, uint64_t* flops_precond);
+
+/* ---- solver (solver.hpp:21-216) ----------------------------------------- */
+/* SolveReport (solver.hpp:48-59) flattened.  defect_history is returned via
+ * the caller's buffer (history_cap rows of k doubles).                      */
+typedef struct {
+  uint64_t iterations;
+  int32_t converged;
+  int32_t breakdown; /* 1 when report.breakdown has a value */
+  uint64_t breakdown_iteration;
+  uint64_t breakdown_block;
+  uint64_t flops_bdot, flops_baxpy, flops_bop, flops_precond; /* FlopCounter   */
+  double seconds_bdot, seconds_baxpy, seconds_bop, seconds_precond; /* KernelSeconds */
+  uint64_t history_rows; /* rows produced (may exceed history_cap)          */
+  double loop_seconds;   /* device time of the iteration loop (CUDA events)  */
+} bkg_report;
+
+/* SolveOptions::on_iterate (solver.hpp:29-31): x and r are HOST copies of
+ * X^i, R^i (n*k row-major), valid during the call only.  Setting it makes the
+ * loop copy X and R back every iteration (the reference semantics).        */
+typedef void (*bkg_iterate_fn)(uint64_t iteration, const double* x, const double* r,
+                               uint64_t n, uint64_t k, void* user);
+
+typedef struct {
+  double tol;          /* SolveOptions::tol       (solver.hpp:24)   */
+  uint64_t max_iter;   /* SolveOptions::max_iter  (0 -> 10 n)       */
+  int32_t record_history;
+  int32_t precond;     /* BKG_PRECOND_*                               */
+  bkg_iterate_fn on_iterate; /* nullable */
+  void* user;
+} bkg_solve_options;
+
+/* bcg_solve (solver.hpp:106-209, X0 = 0 overload :212-216 when x0 == NULL).
+ * Host buffers in, host buffers out; breakdown is reported in *rep, not as a
+ * status (solver.hpp:191-194).                                              */
+int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
+              const double* b, const double* x0, const bkg_solve_options* opts, double* x_out,
+              double* history, uint64_t history_cap, double* final_norms, bkg_report* rep);
+
+/* ---- device-resident solver (bench / repeated solves) ------------------- */
+/* Keeps A, B, X and the work block vectors resident in HBM.                */
+int bkg_solver_create(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
+                      bkg_solver** out);
+int bkg_solver_destroy(bkg_solver* s);
+int bkg_solver_set_rhs(bkg_solver* s, const double* b_host);
+/* Runs a whole solve from X0 = 0 on the resident B.  Host is touched only
+ * every `chunk` iterations to read the stop flag.                          */
+int bkg_solver_run(bkg_solver* s, double tol, uint64_t max_iter, int record_history,
+                   bkg_report* rep);
+int bkg_solver_get_x(bkg_solver* s, double* x_host);
+int bkg_solver_history(bkg_solver* s, double* history, uint64_t cap, uint64_t* rows);
+/* Device time (ms, CUDA events on the solver stream) of each fused kernel
+ * class averaged over `iterations` iterations of an untimed profiling pass:
+ * out_ms[0]=SpMM+Gram (K1), [1]=update+Gram (K2), [2]=P update (K3),
+ * [3]=whole iteration.  Launches are not graph-captured in this pass.      */
+int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms);
+/* Algorithmic bytes one launch of each fused kernel class must move
+ * (DESIGN.md §Roofline): out[0..2] as above, out[3] = per iteration.       */
+int bkg_solver_kernel_bytes(const bkg_solver* s, double* out);
+
+/* ---- problem generators (problems.hpp + frozen new generators) ---------- */
+/* kinds: 0 poisson2d constant, 1 poisson2d log-uniform(seed, contrast),
+ * 2 lognormal 2D diffusion (seed), 3 3D 7-point, 4 3D 27-point.            */
+int bkg_stencil_size(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t* n,
+                     uint64_t* nnz);
+int bkg_stencil_fill(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t seed,
+                     double contrast, uint64_t* row_offsets, uint64_t* cols, double* vals);
+/* random_block_rhs (problems.hpp:128-134) and the frozen N(0,1) stream.   */
+int bkg_random_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out);
+int bkg_normal_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

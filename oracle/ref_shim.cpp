@@ -1,0 +1,199 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrappers around the UNMODIFIED reference blockkrylov headers,
+// compiled straight from /root/reference/proj/include by oracle/Makefile into
+// oracle/_ref/libbkref.so.  Used (a) to pin the C restatement in
+// oracle/bcg_oracle.c bit-for-bit, (b) to generate tests/golden fixtures and
+// (c) as the `kind: "reference"` CPU baseline in bench.py.  Nothing here is a
+// copy of reference source: it only #includes the reference headers.
+#include <blockkrylov/blockkrylov.hpp>
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+using namespace blockkrylov;
+
+namespace {
+
+SubalgebraConfig make_cfg(size_t k, size_t p, int global) {
+  return SubalgebraConfig(k, p, global ? SubalgebraMode::global : SubalgebraMode::hybrid);
+}
+
+BlockVector to_bv(size_t n, size_t k, const double* d) {
+  BlockVector v(n, k);
+  std::memcpy(v.data(), d, n * k * sizeof(double));
+  return v;
+}
+
+SparseMatrix to_csr(size_t n, const uint64_t* rowptr, const uint64_t* cols, const double* vals) {
+  const size_t nnz = rowptr[n];
+  return SparseMatrix(n, std::vector<std::size_t>(rowptr, rowptr + n + 1),
+                      std::vector<std::size_t>(cols, cols + nnz),
+                      std::vector<double>(vals, vals + nnz));
+}
+
+Preconditioner make_precond(int kind, const SparseMatrix& a) {
+  if (kind == 1) return Preconditioner::jacobi(a);
+  if (kind == 2) return ilu0_factor(a);
+  return Preconditioner::identity(a.n());
+}
+
+struct Report {  // same layout as orc_report (bcg_oracle.h)
+  uint64_t iterations;
+  int32_t converged;
+  int32_t breakdown;
+  uint64_t breakdown_iteration;
+  uint64_t breakdown_block;
+  uint64_t flops_bdot, flops_baxpy, flops_bop, flops_precond;
+  double seconds_bdot, seconds_baxpy, seconds_bop, seconds_precond;
+  uint64_t history_rows;
+};
+
+}  // namespace
+
+extern "C" {
+
+void bkref_rng_symmetric(uint64_t seed, size_t count, double* out) {
+  Xorshift64Star g(seed);
+  for (size_t i = 0; i < count; ++i) out[i] = g.next_symmetric();
+}
+
+void bkref_random_block_rhs(size_t n, size_t k, uint64_t seed, double* out) {
+  const BlockVector b = random_block_rhs(n, k, seed);
+  std::memcpy(out, b.data(), n * k * sizeof(double));
+}
+
+// poisson2d (constant when contrast < 0, heterogeneous otherwise); returns nnz.
+size_t bkref_poisson2d(size_t nx, size_t ny, uint64_t seed, double contrast, uint64_t* rowptr,
+                       uint64_t* cols, double* vals) {
+  const SparseMatrix a = contrast < 0 ? poisson2d(PoissonSpec::constant(nx, ny))
+                                      : poisson2d(PoissonSpec::heterogeneous(nx, ny, seed, contrast));
+  if (rowptr) {
+    for (size_t i = 0; i <= a.n(); ++i) rowptr[i] = a.row_offsets()[i];
+    for (size_t i = 0; i < a.nnz(); ++i) {
+      cols[i] = a.col_indices()[i];
+      vals[i] = a.values()[i];
+    }
+  }
+  return a.nnz();
+}
+
+void bkref_bdot(size_t n, size_t k, size_t p, int global, const double* x, const double* y,
+                double* out) {
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  const BlockCoefficient g = bdot(to_bv(n, k, x), to_bv(n, k, y), cfg);
+  for (size_t b = 0; b < g.block_count(); ++b)
+    std::memcpy(out + b * p * p, g.block(b).data(), p * p * sizeof(double));
+}
+
+void bkref_baxpy(size_t n, size_t k, size_t p, int global, double* x, const double* y,
+                 const double* gamma) {
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  BlockCoefficient g(cfg);
+  for (size_t b = 0; b < g.block_count(); ++b)
+    std::memcpy(g.block(b).data(), gamma + b * p * p, p * p * sizeof(double));
+  BlockVector xv = to_bv(n, k, x);
+  baxpy(xv, to_bv(n, k, y), g);
+  std::memcpy(x, xv.data(), n * k * sizeof(double));
+}
+
+void bkref_bop(size_t n, const uint64_t* rowptr, const uint64_t* cols, const double* vals,
+               size_t k, const double* x, double* y) {
+  const BlockVector out = bop(to_csr(n, rowptr, cols, vals), to_bv(n, k, x));
+  std::memcpy(y, out.data(), n * k * sizeof(double));
+}
+
+int bkref_bsolve(size_t k, size_t p, int global, const double* gamma, const double* delta,
+                 double* out, uint64_t* bad_block) {
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  BlockCoefficient g(cfg), d(cfg);
+  for (size_t b = 0; b < g.block_count(); ++b) {
+    std::memcpy(g.block(b).data(), gamma + b * p * p, p * p * sizeof(double));
+    std::memcpy(d.block(b).data(), delta + b * p * p, p * p * sizeof(double));
+  }
+  try {
+    const BlockCoefficient r = bsolve(g, d);
+    for (size_t b = 0; b < r.block_count(); ++b)
+      std::memcpy(out + b * p * p, r.block(b).data(), p * p * sizeof(double));
+    return 0;
+  } catch (const BreakdownError& e) {
+    if (bad_block) *bad_block = e.block_index();
+    return 3;
+  }
+}
+
+void bkref_column_norms(size_t n, size_t k, const double* x, double* out) {
+  const std::vector<double> v = column_norms(to_bv(n, k, x));
+  std::memcpy(out, v.data(), k * sizeof(double));
+}
+
+int bkref_bcg_solve(size_t n, const uint64_t* rowptr, const uint64_t* cols, const double* vals,
+                    int precond_kind, size_t k, size_t p, int global, const double* b,
+                    const double* x0, double tol, uint64_t max_iter, int record_history,
+                    double* history, uint64_t history_cap, double* x_out, double* final_norms,
+                    Report* rep) {
+  const SparseMatrix a = to_csr(n, rowptr, cols, vals);
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  SolveOptions opts;
+  opts.tol = tol;
+  opts.max_iter = max_iter;
+  opts.record_history = record_history != 0;
+  const Preconditioner m = make_precond(precond_kind, a);
+  const BlockVector bv = to_bv(n, k, b);
+  const SolveResult res = x0 ? bcg_solve(a, bv, to_bv(n, k, x0), m, cfg, opts)
+                             : bcg_solve(a, bv, m, cfg, opts);
+  std::memcpy(x_out, res.x.data(), n * k * sizeof(double));
+  if (final_norms)
+    std::memcpy(final_norms, res.report.final_defect_norms.data(), k * sizeof(double));
+  std::memset(rep, 0, sizeof(*rep));
+  rep->iterations = res.report.iterations;
+  rep->converged = res.report.converged;
+  rep->breakdown = res.report.breakdown.has_value();
+  if (res.report.breakdown) {
+    rep->breakdown_iteration = res.report.breakdown->iteration;
+    rep->breakdown_block = res.report.breakdown->block_index;
+  }
+  rep->flops_bdot = res.report.flops.multiply_adds_bdot;
+  rep->flops_baxpy = res.report.flops.multiply_adds_baxpy;
+  rep->flops_bop = res.report.flops.multiply_adds_bop;
+  rep->flops_precond = res.report.flops.multiply_adds_precond;
+  rep->seconds_bdot = res.report.seconds.bdot;
+  rep->seconds_baxpy = res.report.seconds.baxpy;
+  rep->seconds_bop = res.report.seconds.bop;
+  rep->seconds_precond = res.report.seconds.precond;
+  rep->history_rows = res.report.defect_history.size();
+  for (size_t i = 0; i < res.report.defect_history.size() && i < history_cap; ++i)
+    std::memcpy(history + i * k, res.report.defect_history[i].data(), k * sizeof(double));
+  return 0;
+}
+
+// CPU baseline: `threads` independent reference solves (one per thread) of the
+// same system, each capped at max_iter.  Returns wall seconds of the solves.
+double bkref_bench_solve(int threads, size_t n, const uint64_t* rowptr, const uint64_t* cols,
+                         const double* vals, size_t k, size_t p, int global, const double* b,
+                         double tol, uint64_t max_iter, uint64_t* iterations) {
+  const SparseMatrix a = to_csr(n, rowptr, cols, vals);
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  const BlockVector bv = to_bv(n, k, b);
+  const Preconditioner m = Preconditioner::identity(n);
+  SolveOptions opts;
+  opts.tol = tol;
+  opts.max_iter = max_iter;
+  if (threads < 1) threads = 1;
+  std::vector<uint64_t> its(threads, 0);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] { its[t] = bcg_solve(a, bv, m, cfg, opts).report.iterations; });
+  for (auto& th : pool) th.join();
+  const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  uint64_t total = 0;
+  for (auto v : its) total += v;
+  if (iterations) *iterations = total;
+  return dt;
+}
+
+}  // extern "C"

@@ -1,0 +1,957 @@
+// api.cu — C ABI (include/bkg.h) and the device-resident Block-CG loop.
+//
+// Host orchestration only: every arithmetic step of the hot path runs in the
+// sm_100a kernels of kernels_fast.cuh / kernels_exact.cuh / bsolve.cuh.  There
+// is no CPU fallback; without a device every call fails with BKG_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bkg.h"
+#include "bsolve.cuh"
+#include "common.cuh"
+#include "fast_table.cuh"
+#include "kernels_exact.cuh"
+#include "kernels_fast.cuh"
+#include "precond.cuh"
+
+namespace bkg {
+
+thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return BKG_OK;
+  } catch (const Error& e) {
+    set_error(e.msg());
+    return e.code();
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return BKG_INTERNAL;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return BKG_INTERNAL;
+  }
+}
+
+// ------------------------------------------------ exact-mode solve steps ---
+// lambda = alpha^-1 rho_prev and -lambda (solver.hpp:170-175).
+__global__ void k_exact_lambda(Ctrl* ctrl, int nblk, int p, double* coef, int cs) {
+  if (stopped(ctrl)) return;
+  extern __shared__ double ws[];
+  const int bad = cta_bsolve<0>(nblk, p, coef + 4 * cs, coef + cs, coef, ws);
+  if (bad >= 0) {
+    record_breakdown(ctrl, bad, 1);
+    return;
+  }
+  for (int i = threadIdx.x; i < cs; i += blockDim.x) coef[5 * cs + i] = -coef[i];
+}
+
+// beta = rho_prev^-1 rho, then history / stop test (solver.hpp:185-200).
+__global__ void k_exact_beta(Ctrl* ctrl, int nblk, int p, int k, double* coef, int cs,
+                             const double* norms, const double* limits, double* hist, int ring) {
+  if (stopped(ctrl)) return;
+  extern __shared__ double ws[];
+  const int bad = cta_bsolve<0>(nblk, p, coef + cs, coef + 3 * cs, coef + 2 * cs, ws);
+  if (bad >= 0) {
+    record_breakdown(ctrl, bad, 2);
+    return;
+  }
+  finish_iteration(ctrl, norms, limits, hist, ring, k);
+}
+
+// ------------------------------------------------------------ helpers -----
+void activate(bkg_ctx* c) { BKG_CUDA_CHECK(cudaSetDevice(c->device)); }
+
+int elem_grid(const bkg_ctx* c, int64_t total) {
+  const int64_t need = (total + 255) / 256;
+  const int64_t cap = (int64_t)c->sm_count * 16;
+  return (int)std::max<int64_t>(1, std::min(need, cap));
+}
+
+void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void** args) {
+  BKG_CUDA_CHECK(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, c->stream));
+  c->launches++;
+}
+
+void allow_smem(const void* fn, int bytes) {
+  if (bytes > 48 * 1024)
+    BKG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc) {
+  int nb = 0;
+  allow_smem(fn, smem);
+  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem));
+  if (nb < 1) nb = 1;
+  const int64_t need = std::max<int64_t>(1, (rows + rpc - 1) / rpc);
+  return (int)std::min<int64_t>((int64_t)nb * c->sm_count, need);
+}
+
+// Reduction scratch (partials, group partials, tickets) owned by a context.
+struct Scratch {
+  double* partials;
+  double* gpart;
+  Ctrl* ctrl;
+};
+
+Scratch ctx_scratch(bkg_ctx* c, int grid, int entries) {
+  const size_t need = (size_t)(grid + kMaxTicketGroups) * entries;
+  c->scratch.ensure(need);
+  if (c->ctrl.count < sizeof(Ctrl)) {
+    c->ctrl.alloc(sizeof(Ctrl));
+    BKG_CUDA_CHECK(cudaMemsetAsync(c->ctrl.ptr, 0, sizeof(Ctrl), c->stream));
+  }
+  return {c->scratch.ptr, c->scratch.ptr + (size_t)grid * entries,
+          reinterpret_cast<Ctrl*>(c->ctrl.ptr)};
+}
+
+bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t) {
+  if (c->numerics != BKG_NUMERICS_FAST) return false;
+  return fast_lookup(k, p, global, t);
+}
+
+void check_cfg(uint64_t k, uint64_t p, int mode) {
+  BKG_REQUIRE(k > 0 && p > 0, BKG_CONFIG, "subalgebra: k and p must be positive");
+  BKG_REQUIRE(k % p == 0, BKG_CONFIG,
+              "subalgebra: block width p=" + std::to_string(p) + " does not divide k=" +
+                  std::to_string(k));
+  BKG_REQUIRE(mode == BKG_HYBRID || mode == BKG_GLOBAL, BKG_CONFIG, "unknown subalgebra mode");
+  BKG_REQUIRE(k <= (1u << 20), BKG_CONFIG, "k too large");
+}
+
+// ---- device-pointer building blocks (shared by the ABI and the solver) ---
+void dev_spmm(bkg_ctx* c, const bkg_matrix* A, int k, const double* x, double* y,
+              const Ctrl* ctrl = nullptr, bool force_exact = false) {
+  FastTable t;
+  const int64_t n = (int64_t)A->n;
+  if (!force_exact && ctrl == nullptr && use_fast(c, k, 1, false, &t)) {
+    VecArgs a{};
+    a.n = n;
+    a.rowptr = A->rowptr.ptr;
+    a.cols = A->cols.ptr;
+    a.vals = A->vals.ptr;
+    a.x = x;
+    a.out = y;
+    void* args[] = {&a};
+    launch(c, t.spmm, occupancy_grid(c, t.spmm, 0, n, kThreads / (k / t.cpt)), kThreads, 0, args);
+    return;
+  }
+  int64_t nn = n;
+  int kk = k;
+  const int64_t* rp = A->rowptr.ptr;
+  const int32_t* cl = A->cols.ptr;
+  const double* vl = A->vals.ptr;
+  void* args[] = {&ctrl, &nn, &kk, &rp, &cl, &vl, &x, &y};
+  launch(c, (const void*)&k_spmm_exact, elem_grid(c, n * k), 256, 0, args);
+}
+
+void dev_baxpy(bkg_ctx* c, int64_t n, int k, int p, bool global, double* x, const double* y,
+               const double* gamma, const Ctrl* ctrl = nullptr, bool force_exact = false) {
+  FastTable t;
+  if (!force_exact && ctrl == nullptr && use_fast(c, k, p, global, &t)) {
+    VecArgs a{};
+    a.n = n;
+    a.y = y;
+    a.out = x;
+    a.coef = gamma;
+    void* args[] = {&a};
+    launch(c, t.baxpy, occupancy_grid(c, t.baxpy, 0, n, t.rpc), kThreads, 0, args);
+    return;
+  }
+  int kk = k, pp = p, gl = global ? 1 : 0;
+  void* args[] = {&ctrl, &n, &kk, &pp, &gl, &x, &y, &gamma};
+  launch(c, (const void*)&k_baxpy_exact, elem_grid(c, n * k), 256, 0, args);
+}
+
+// Gram (BDOT) or column norms into a device buffer.
+void dev_chain(bkg_ctx* c, bool norms, int64_t n, int k, int p, bool global, const double* x,
+               const double* y, double* out, const Ctrl* ctrl) {
+  const int nblk = global ? 1 : k / p;
+  int entries = norms ? k : nblk * p * p;
+  const int smem = (int)chain_smem_bytes(k, norms);
+  const void* fn = norms ? (const void*)&k_chain_exact<true> : (const void*)&k_chain_exact<false>;
+  allow_smem(fn, smem);
+  int kk = k, pp = p, gl = global ? 1 : 0;
+  void* args[] = {&ctrl, &n, &kk, &pp, &gl, &entries, &x, &y, &out};
+  launch(c, fn, (entries + kChainThreads - 1) / kChainThreads, kChainThreads, smem, args);
+}
+
+void dev_gram(bkg_ctx* c, int64_t n, int k, int p, bool global, const double* x,
+              const double* y, double* out, bool force_exact = false) {
+  FastTable t;
+  if (!force_exact && n > 0 && use_fast(c, k, p, global, &t)) {
+    const int grid = occupancy_grid(c, t.gram, t.smem_gram, n, t.rpc);
+    Scratch s = ctx_scratch(c, grid, t.e_gram);
+    VecArgs a{};
+    a.n = n;
+    a.x = x;
+    a.y = y;
+    a.out = out;
+    a.partials = s.partials;
+    a.gpart = s.gpart;
+    a.tickets = s.ctrl->tickets;
+    void* args[] = {&a};
+    launch(c, t.gram, grid, kThreads, t.smem_gram, args);
+    return;
+  }
+  dev_chain(c, false, n, k, p, global, x, y, out, nullptr);
+}
+
+void dev_norms(bkg_ctx* c, int64_t n, int k, const double* x, double* out,
+               bool force_exact = false) {
+  FastTable t;
+  if (!force_exact && n > 0 && use_fast(c, k, 1, false, &t)) {
+    const int grid = occupancy_grid(c, t.norms, t.smem_norms, n, kThreads / (k / t.cpt));
+    Scratch s = ctx_scratch(c, grid, t.e_norms);
+    VecArgs a{};
+    a.n = n;
+    a.x = x;
+    a.out = out;
+    a.partials = s.partials;
+    a.gpart = s.gpart;
+    a.tickets = s.ctrl->tickets;
+    void* args[] = {&a};
+    launch(c, t.norms, grid, kThreads, t.smem_norms, args);
+    return;
+  }
+  dev_chain(c, true, n, k, 1, false, x, x, out, nullptr);
+}
+
+int dev_bsolve(bkg_ctx* c, int nblk, int p, const double* gamma, const double* delta,
+               double* out, int* status) {
+  const int smem = (int)sizeof(double) * bsolve_ws_doubles(p, 256);
+  const void* fn = (const void*)&k_bsolve<0>;
+  allow_smem(fn, smem);
+  void* args[] = {&nblk, &p, &gamma, &delta, &out, &status};
+  launch(c, fn, 1, 256, smem, args);
+  return 0;
+}
+
+template <class T>
+void h2d(bkg_ctx* c, T* dst, const T* src, size_t count) {
+  if (count) BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+}
+template <class T>
+void d2h(bkg_ctx* c, T* dst, const T* src, size_t count) {
+  if (count) BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+void sync(bkg_ctx* c) { BKG_CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
+
+__global__ void k_u64_to_i32(int64_t count, const uint64_t* __restrict__ src,
+                             int32_t* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (int32_t)src[i];
+}
+
+}  // namespace bkg
+
+using namespace bkg;
+
+// =========================================================== solver =====
+struct bkg_solver {
+  bkg_ctx* ctx = nullptr;
+  const bkg_matrix* A = nullptr;
+  int64_t n = 0;
+  int k = 0, p = 0;
+  bool global = false;
+  int nblk = 0, cs = 0;
+  bool fast = false;
+  FastTable ft;
+  int g1 = 1, g2 = 1, g3 = 1;
+  int ring = 66, chunk = 32;
+  DevBuf<double> B, X, R, Q, Pb, Zb, coef, limits, hist, norms, partials, gpart;
+  DevBuf<char> ctrl_buf;
+  Ctrl* h_ctrl = nullptr;
+  double* h_ring = nullptr;
+  double* P = nullptr;  // current P (exact mode ping-pongs P / Z)
+  double* Z = nullptr;
+  bool have_b = false;
+  int precond = BKG_PRECOND_IDENTITY;
+  std::vector<double> history;  // rows x k
+  uint64_t history_rows = 0;
+
+  Ctrl* dctrl() { return reinterpret_cast<Ctrl*>(ctrl_buf.ptr); }
+
+  ~bkg_solver() {
+    if (h_ctrl) cudaFreeHost(h_ctrl);
+    if (h_ring) cudaFreeHost(h_ring);
+  }
+
+  void init(bkg_ctx* c, const bkg_matrix* a, int kk, int pp, bool gl) {
+    ctx = c;
+    A = a;
+    n = (int64_t)a->n;
+    k = kk;
+    p = pp;
+    global = gl && pp != kk;  // global with p = k is classical (test_kernels.cpp:131-140)
+    nblk = global ? 1 : k / p;
+    cs = nblk * p * p;
+    fast = use_fast(c, k, p, global, &ft);
+    const size_t nk = (size_t)n * k;
+    B.alloc(nk);
+    X.alloc(nk);
+    R.alloc(nk);
+    Q.alloc(nk);
+    Pb.alloc(nk);
+    if (!fast) Zb.alloc(nk);
+    P = Pb.ptr;
+    Z = Zb.ptr;
+    coef.alloc((size_t)6 * cs);
+    limits.alloc(k);
+    norms.alloc(k);
+    hist.alloc((size_t)ring * k);
+    ctrl_buf.alloc(sizeof(Ctrl));
+    BKG_CUDA_CHECK(cudaMemsetAsync(ctrl_buf.ptr, 0, sizeof(Ctrl), c->stream));
+    BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
+    BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
+    if (fast) {
+      g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc);
+      g2 = occupancy_grid(c, ft.k2, ft.smem_iter, n, ft.rpc);
+      g3 = occupancy_grid(c, ft.k3, 0, n, ft.rpc);
+      const int gmax = std::max(g1, g2);
+      partials.alloc((size_t)gmax * ft.e_iter);
+      gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
+    }
+  }
+
+  IterArgs iter_args(bool with_hist) {
+    IterArgs a{};
+    a.n = n;
+    a.rowptr = A->rowptr.ptr;
+    a.cols = A->cols.ptr;
+    a.vals = A->vals.ptr;
+    a.X = X.ptr;
+    a.R = R.ptr;
+    a.P = P;
+    a.Q = Q.ptr;
+    a.partials = partials.ptr;
+    a.gpart = gpart.ptr;
+    a.coef = coef.ptr;
+    a.limits = limits.ptr;
+    a.hist = with_hist ? hist.ptr : nullptr;
+    a.hist_ring = ring;
+    a.group = 16;
+    a.ctrl = dctrl();
+    return a;
+  }
+
+  // One Block-CG iteration (solver.hpp:157-201), queued on the ctx stream.
+  void launch_iteration(bool with_hist, cudaEvent_t* ev = nullptr) {
+    Ctrl* ctrl = dctrl();
+    if (fast) {
+      IterArgs a = iter_args(with_hist);
+      void* args[] = {&a};
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
+      launch(ctx, ft.k1, g1, kThreads, ft.smem_iter, args);
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
+      launch(ctx, ft.k2, g2, kThreads, ft.smem_iter, args);
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
+      launch(ctx, ft.k3, g3, kThreads, 0, args);
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
+      return;
+    }
+    const Ctrl* cc = ctrl;
+    double* cf = coef.ptr;
+    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
+    dev_spmm(ctx, A, k, P, Q.ptr, cc, true);                                  // Q = A P
+    dev_chain(ctx, false, n, k, p, global, P, Q.ptr, cf + 4 * cs, cc);        // alpha
+    dev_chain(ctx, false, n, k, p, global, P, R.ptr, cf + cs, cc);            // rho_prev
+    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
+    {
+      const int smem = (int)sizeof(double) * bsolve_ws_doubles(p, 256);
+      allow_smem((const void*)&k_exact_lambda, smem);
+      int nb = nblk, pp = p, c_s = cs;
+      void* args[] = {&ctrl, &nb, &pp, &cf, &c_s};
+      launch(ctx, (const void*)&k_exact_lambda, 1, 256, smem, args);
+    }
+    dev_baxpy(ctx, n, k, p, global, X.ptr, P, cf, cc, true);                  // X += P lambda
+    dev_baxpy(ctx, n, k, p, global, R.ptr, Q.ptr, cf + 5 * cs, cc, true);     // R -= Q lambda
+    {
+      int64_t tot = n * k;
+      const double* src = R.ptr;
+      double* dst = Z;
+      void* args[] = {&cc, &tot, &src, &dst};
+      launch(ctx, (const void*)&k_copy, elem_grid(ctx, tot), 256, 0, args);  // Z = M^-1 R
+    }
+    dev_chain(ctx, false, n, k, p, global, Z, R.ptr, cf + 3 * cs, cc);        // rho
+    dev_chain(ctx, true, n, k, 1, false, R.ptr, R.ptr, norms.ptr, cc);        // ||R_s||
+    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
+    {
+      const int smem = (int)sizeof(double) * bsolve_ws_doubles(p, 256);
+      allow_smem((const void*)&k_exact_beta, smem);
+      int nb = nblk, pp = p, kk = k, c_s = cs, rg = ring;
+      const double* nm = norms.ptr;
+      const double* lm = limits.ptr;
+      double* hs = with_hist ? hist.ptr : nullptr;
+      void* args[] = {&ctrl, &nb, &pp, &kk, &cf, &c_s, &nm, &lm, &hs, &rg};
+      launch(ctx, (const void*)&k_exact_beta, 1, 256, smem, args);
+    }
+    dev_baxpy(ctx, n, k, p, global, Z, P, cf + 2 * cs, cc, true);             // Z += P beta
+    std::swap(P, Z);                                                           // P^{i+1}
+    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
+  }
+
+  bool norms_fast() const { return fast; }
+
+  // Setup of a solve: X0, R0, limits, initial history row (solver.hpp:121-155).
+  // Returns true when R0 already satisfies the stop test.
+  bool setup(const double* x0_host, double tol, uint64_t max_iter, bool record,
+             bkg_report* rep, std::vector<double>* limits_host, bool* x0_nonzero) {
+    const size_t nk = (size_t)n * k;
+    bool x0_zero = true;
+    if (x0_host) {
+      for (size_t i = 0; i < nk && x0_zero; ++i) x0_zero = x0_host[i] == 0.0;
+    }
+    *x0_nonzero = !x0_zero;
+    if (x0_zero)
+      BKG_CUDA_CHECK(cudaMemsetAsync(X.ptr, 0, nk * sizeof(double), ctx->stream));
+    else
+      h2d(ctx, X.ptr, x0_host, nk);
+    BKG_CUDA_CHECK(cudaMemcpyAsync(R.ptr, B.ptr, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (!x0_zero) {  // R = B - A X0 via bop + baxpy(-I) (solver.hpp:127-139)
+      dev_spmm(ctx, A, k, X.ptr, Q.ptr, nullptr, true);
+      std::vector<double> neg((size_t)cs, -0.0);
+      for (int b = 0; b < nblk; ++b)
+        for (int i = 0; i < p; ++i) neg[(size_t)b * p * p + i * p + i] = -1.0;
+      h2d(ctx, coef.ptr + 5 * cs, neg.data(), cs);
+      dev_baxpy(ctx, n, k, p, global, R.ptr, Q.ptr, coef.ptr + 5 * cs, nullptr, true);
+      rep->flops_bop += 2ull * k * A->nnz;
+      rep->flops_baxpy += 2ull * n * p * p * (k / p);
+    }
+    std::vector<double> bn(k), rn(k);
+    dev_norms(ctx, n, k, B.ptr, norms.ptr, !norms_fast());
+    d2h(ctx, bn.data(), norms.ptr, k);
+    sync(ctx);
+    limits_host->resize(k);
+    for (int s = 0; s < k; ++s) (*limits_host)[s] = bn[s] > 0.0 ? tol * bn[s] : tol;
+    h2d(ctx, limits.ptr, limits_host->data(), k);
+    dev_norms(ctx, n, k, R.ptr, norms.ptr, !norms_fast());
+    d2h(ctx, rn.data(), norms.ptr, k);
+    sync(ctx);
+    history.clear();
+    history_rows = 0;
+    if (record) {
+      history.insert(history.end(), rn.begin(), rn.end());
+      history_rows = 1;
+    }
+    bool conv = true;
+    for (int s = 0; s < k; ++s)
+      if (!(rn[s] <= (*limits_host)[s])) conv = false;
+    Ctrl h{};
+    h.done = conv ? 1 : 0;
+    h.converged = conv ? 1 : 0;
+    h.max_iter = max_iter;
+    h2d(ctx, reinterpret_cast<char*>(dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
+    P = Pb.ptr;
+    Z = Zb.ptr;
+    if (!conv)  // P^1 = M^-1 R^0 (identity: copy, solver.hpp:152-155)
+      BKG_CUDA_CHECK(cudaMemcpyAsync(P, R.ptr, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    return conv;
+  }
+
+  // The device-resident loop.  The host only reads the control block every
+  // `chunk` iterations (every iteration when an observer is attached).
+  void loop(bool record, bkg_iterate_fn cb, void* user, double* loop_seconds) {
+    const size_t nk = (size_t)n * k;
+    std::vector<double> hx, hr;
+    if (cb) {
+      hx.resize(nk);
+      hr.resize(nk);
+    }
+    cudaEvent_t e0, e1;
+    BKG_CUDA_CHECK(cudaEventCreate(&e0));
+    BKG_CUDA_CHECK(cudaEventCreate(&e1));
+    BKG_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+    d2h(ctx, reinterpret_cast<char*>(h_ctrl), reinterpret_cast<const char*>(dctrl()), sizeof(Ctrl));
+    sync(ctx);
+    uint64_t seen = 0;
+    while (!h_ctrl->done) {
+      const int c = cb ? 1 : chunk;
+      for (int i = 0; i < c; ++i) launch_iteration(record);
+      d2h(ctx, reinterpret_cast<char*>(h_ctrl), reinterpret_cast<const char*>(dctrl()), sizeof(Ctrl));
+      if (record) d2h(ctx, h_ring, hist.ptr, (size_t)ring * k);
+      if (cb) {
+        d2h(ctx, hx.data(), X.ptr, nk);
+        d2h(ctx, hr.data(), R.ptr, nk);
+      }
+      sync(ctx);
+      const uint64_t it = h_ctrl->iterations;
+      if (record) {
+        for (uint64_t i = seen + 1; i <= it; ++i) {
+          const double* row = h_ring + (size_t)(i % ring) * k;
+          history.insert(history.end(), row, row + k);
+          ++history_rows;
+        }
+      }
+      if (cb && it > seen) cb(it, hx.data(), hr.data(), (uint64_t)n, (uint64_t)k, user);
+      seen = it;
+    }
+    BKG_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+    BKG_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    BKG_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    *loop_seconds = 1e-3 * ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+
+  void final_residual(double* final_norms_host) {  // solver.hpp:203-207
+    const int64_t nk = n * (int64_t)k;
+    dev_spmm(ctx, A, k, X.ptr, Q.ptr, nullptr, !fast);
+    const double* b = B.ptr;
+    double* q = Q.ptr;
+    int64_t tot = nk;
+    void* args[] = {&tot, &b, &q};
+    launch(ctx, (const void*)&k_residual_exact, elem_grid(ctx, tot), 256, 0, args);
+    dev_norms(ctx, n, k, Q.ptr, norms.ptr, !fast);
+    if (final_norms_host) d2h(ctx, final_norms_host, norms.ptr, k);
+  }
+
+  void fill_report(bkg_report* rep, bool conv0) {
+    const Ctrl& h = *h_ctrl;
+    rep->iterations = h.iterations;
+    rep->converged = h.converged;
+    rep->breakdown = h.breakdown;
+    rep->breakdown_iteration = h.breakdown_iteration;
+    rep->breakdown_block = h.breakdown_block;
+    const uint64_t it = h.iterations;
+    const uint64_t bdot1 = 2ull * n * p * p * (k / p);
+    const uint64_t bop1 = 2ull * k * A->nnz;
+    uint64_t bops = it, bdots = 3 * it, baxpys = 3 * it;
+    if (h.breakdown) {
+      bops += 1;
+      bdots += h.stage == 1 ? 2 : 3;
+      baxpys += h.stage == 1 ? 0 : 2;
+    }
+    (void)conv0;
+    rep->flops_bdot += bdots * bdot1;
+    rep->flops_baxpy += baxpys * bdot1;
+    rep->flops_bop += bops * bop1;
+    rep->history_rows = history_rows;
+  }
+
+  void run(const double* x0_host, double tol, uint64_t max_iter_opt, bool record,
+           bkg_iterate_fn cb, void* user, double* final_norms, bkg_report* rep) {
+    BKG_REQUIRE(have_b, BKG_CONFIG, "solver: right hand side not set");
+    BKG_REQUIRE(tol > 0.0, BKG_CONFIG, "bcg_solve: tol must be positive");
+    std::memset(rep, 0, sizeof(*rep));
+    const uint64_t max_iter = max_iter_opt ? max_iter_opt : 10ull * (uint64_t)n;
+    std::vector<double> lim;
+    bool x0nz = false;
+    const bool conv0 = setup(x0_host, tol, max_iter, record, rep, &lim, &x0nz);
+    if (cb) {
+      const size_t nk = (size_t)n * k;
+      std::vector<double> hx(nk), hr(nk);
+      d2h(ctx, hx.data(), X.ptr, nk);
+      d2h(ctx, hr.data(), R.ptr, nk);
+      sync(ctx);
+      cb(0, hx.data(), hr.data(), (uint64_t)n, (uint64_t)k, user);
+    }
+    loop(record, cb, user, &rep->loop_seconds);
+    fill_report(rep, conv0);
+    final_residual(final_norms);
+    sync(ctx);
+  }
+};
+
+// =========================================================== ABI ========
+extern "C" {
+
+const char* bkg_last_error(void) { return bkg::last_error(); }
+const char* bkg_version(void) { return "bkg 0.1 (sm_100a)"; }
+
+int bkg_device_count(int* count) {
+  return guard([&] {
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    *count = e == cudaSuccess ? c : 0;
+    cudaGetLastError();
+  });
+}
+
+int bkg_ctx_create(int device, bkg_ctx** out) {
+  return guard([&] {
+    *out = nullptr;
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    BKG_REQUIRE(e == cudaSuccess && count > 0, BKG_CUDA,
+                std::string("no CUDA device available (") + cudaGetErrorString(e) + ")");
+    BKG_REQUIRE(device >= 0 && device < count, BKG_CUDA, "device index out of range");
+    BKG_CUDA_CHECK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    BKG_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    BKG_REQUIRE(prop.major >= 10, BKG_CUDA,
+                std::string("libbkgpu is built for sm_100a; device is ") + prop.name);
+    auto* c = new bkg_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    BKG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int bkg_ctx_destroy(bkg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->scratch.release();
+    ctx->ctrl.release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int bkg_ctx_set_numerics(bkg_ctx* ctx, int numerics) {
+  return guard([&] {
+    BKG_REQUIRE(numerics == BKG_NUMERICS_FAST || numerics == BKG_NUMERICS_EXACT, BKG_CONFIG,
+                "unknown numerics mode");
+    ctx->numerics = numerics;
+  });
+}
+
+int bkg_ctx_get_numerics(const bkg_ctx* ctx, int* numerics) {
+  return guard([&] { *numerics = ctx->numerics; });
+}
+
+int bkg_ctx_stream(const bkg_ctx* ctx, void** stream) {
+  return guard([&] { *stream = (void*)ctx->stream; });
+}
+
+int bkg_ctx_launch_count(const bkg_ctx* ctx, uint64_t* launches) {
+  return guard([&] { *launches = ctx->launches; });
+}
+
+int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint64_t* cols,
+                      const double* vals, bkg_matrix** out) {
+  return guard([&] {
+    *out = nullptr;
+    // structural checks of sparse_matrix.hpp:89-105 (value symmetry is the
+    // host SparseMatrix constructor's job)
+    BKG_REQUIRE(n > 0, BKG_CONFIG, "sparse matrix: dimension must be positive");
+    BKG_REQUIRE(n < (1ull << 31), BKG_CONFIG, "sparse matrix: n must be < 2^31 on device");
+    BKG_REQUIRE(off[0] == 0, BKG_CONFIG, "sparse matrix: offsets inconsistent with stored entries");
+    const uint64_t nnz = off[n];
+    for (uint64_t r = 0; r < n; ++r) {
+      BKG_REQUIRE(off[r] <= off[r + 1], BKG_CONFIG, "sparse matrix: row_offsets must be non-decreasing");
+      for (uint64_t i = off[r]; i < off[r + 1]; ++i) {
+        BKG_REQUIRE(cols[i] < n, BKG_CONFIG, "sparse matrix: column index out of range");
+        BKG_REQUIRE(i == off[r] || cols[i] > cols[i - 1], BKG_CONFIG,
+                    "sparse matrix: columns must be strictly ascending per row");
+      }
+    }
+    activate(ctx);
+    auto* m = new bkg_matrix();
+    m->ctx = ctx;
+    m->n = n;
+    m->nnz = nnz;
+    try {
+      m->rowptr.alloc(n + 1);
+      m->cols.alloc(std::max<uint64_t>(nnz, 1));
+      m->vals.alloc(std::max<uint64_t>(nnz, 1));
+      h2d(ctx, reinterpret_cast<uint64_t*>(m->rowptr.ptr), off, n + 1);
+      h2d(ctx, m->vals.ptr, vals, nnz);
+      if (nnz) {
+        DevBuf<uint64_t> tmp(nnz);
+        h2d(ctx, tmp.ptr, cols, nnz);
+        int64_t cnt = (int64_t)nnz;
+        const uint64_t* s = tmp.ptr;
+        int32_t* d = m->cols.ptr;
+        void* args[] = {&cnt, &s, &d};
+        launch(ctx, (const void*)&k_u64_to_i32, elem_grid(ctx, cnt), 256, 0, args);
+        sync(ctx);
+      }
+      sync(ctx);
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+int bkg_matrix_destroy(bkg_matrix* m) {
+  return guard([&] {
+    if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    delete m;
+  });
+}
+
+int bkg_matrix_info(const bkg_matrix* m, uint64_t* n, uint64_t* nnz) {
+  return guard([&] {
+    *n = m->n;
+    *nnz = m->nnz;
+  });
+}
+
+int bkg_bdot(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, const double* x,
+             const double* y, double* out, uint64_t* flops) {
+  return guard([&] {
+    check_cfg(k, p, mode);
+    activate(ctx);
+    const bool global = mode == BKG_GLOBAL && p != k;
+    const int nblk = global ? 1 : (int)(k / p);
+    const size_t cs = (size_t)nblk * p * p;
+    if (n == 0) {
+      std::fill(out, out + cs, 0.0);
+    } else {
+      DevBuf<double> dx(n * k), dy(n * k), dout(cs);
+      h2d(ctx, dx.ptr, x, n * k);
+      h2d(ctx, dy.ptr, y, n * k);
+      dev_gram(ctx, (int64_t)n, (int)k, (int)p, global, dx.ptr, dy.ptr, dout.ptr);
+      d2h(ctx, out, dout.ptr, cs);
+      sync(ctx);
+    }
+    if (flops) *flops += 2ull * n * p * p * (k / p);
+  });
+}
+
+int bkg_baxpy(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, double* x,
+              const double* y, const double* gamma, uint64_t* flops) {
+  return guard([&] {
+    check_cfg(k, p, mode);
+    activate(ctx);
+    const bool global = mode == BKG_GLOBAL && p != k;
+    const int nblk = global ? 1 : (int)(k / p);
+    const size_t cs = (size_t)nblk * p * p;
+    if (n > 0) {
+      DevBuf<double> dx(n * k), dy(n * k), dg(cs);
+      h2d(ctx, dx.ptr, x, n * k);
+      h2d(ctx, dy.ptr, y, n * k);
+      h2d(ctx, dg.ptr, gamma, cs);
+      dev_baxpy(ctx, (int64_t)n, (int)k, (int)p, global, dx.ptr, dy.ptr, dg.ptr);
+      d2h(ctx, x, dx.ptr, n * k);
+      sync(ctx);
+    }
+    if (flops) *flops += 2ull * n * p * p * (k / p);
+  });
+}
+
+int bkg_bop(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, const double* x, double* y,
+            uint64_t* flops) {
+  return guard([&] {
+    BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
+    activate(ctx);
+    const uint64_t n = a->n;
+    DevBuf<double> dx(n * k), dy(n * k);
+    h2d(ctx, dx.ptr, x, n * k);
+    dev_spmm(ctx, a, (int)k, dx.ptr, dy.ptr);
+    d2h(ctx, y, dy.ptr, n * k);
+    sync(ctx);
+    if (flops) *flops += 2ull * k * a->nnz;
+  });
+}
+
+int bkg_bsolve(bkg_ctx* ctx, uint64_t k, uint64_t p, int mode, const double* gamma,
+               const double* delta, double* out, uint64_t* bad_block) {
+  int bad = -1;
+  const int st = guard([&] {
+    check_cfg(k, p, mode);
+    BKG_REQUIRE(p <= 1024, BKG_CONFIG, "bsolve: block width too large for the device solver");
+    activate(ctx);
+    const bool global = mode == BKG_GLOBAL && p != k;
+    const int nblk = global ? 1 : (int)(k / p);
+    const size_t cs = (size_t)nblk * p * p;
+    DevBuf<double> dg(cs), dd(cs), dout(cs);
+    DevBuf<int> dst(1);
+    h2d(ctx, dg.ptr, gamma, cs);
+    h2d(ctx, dd.ptr, delta, cs);
+    dev_bsolve(ctx, nblk, (int)p, dg.ptr, dd.ptr, dout.ptr, dst.ptr);
+    d2h(ctx, &bad, dst.ptr, 1);
+    sync(ctx);
+    if (bad < 0) {
+      BKG_CUDA_CHECK(cudaMemcpy(out, dout.ptr, cs * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+  });
+  if (st != BKG_OK) return st;
+  if (bad >= 0) {
+    if (bad_block) *bad_block = (uint64_t)bad;
+    set_error("bsolve: block " + std::to_string(bad) + " is numerically singular");
+    return BKG_BREAKDOWN;
+  }
+  return BKG_OK;
+}
+
+int bkg_column_norms(bkg_ctx* ctx, uint64_t n, uint64_t k, const double* x, double* out) {
+  return guard([&] {
+    BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
+    activate(ctx);
+    if (n == 0) {
+      std::fill(out, out + k, 0.0);
+      return;
+    }
+    DevBuf<double> dx(n * k), dout(k);
+    h2d(ctx, dx.ptr, x, n * k);
+    dev_norms(ctx, (int64_t)n, (int)k, dx.ptr, dout.ptr);
+    d2h(ctx, out, dout.ptr, k);
+    sync(ctx);
+  });
+}
+
+int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k,
+                      const double* r, double* z, uint64_t* flops) {
+  return guard([&] {
+    BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
+    activate(ctx);
+    const uint64_t n = a->n;
+    DevBuf<double> dr(n * k), dz(n * k);
+    h2d(ctx, dr.ptr, r, n * k);
+    const uint64_t f = precond_apply_dev(ctx, const_cast<bkg_matrix*>(a), precond, (int)k,
+                                         dr.ptr, dz.ptr, nullptr);
+    d2h(ctx, z, dz.ptr, n * k);
+    sync(ctx);
+    if (flops) *flops += f;
+  });
+}
+
+int bkg_solver_create(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
+                      bkg_solver** out) {
+  return guard([&] {
+    *out = nullptr;
+    check_cfg(k, p, mode);
+    activate(ctx);
+    auto* s = new bkg_solver();
+    try {
+      s->init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int bkg_solver_destroy(bkg_solver* s) {
+  return guard([&] {
+    if (!s) return;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    delete s;
+  });
+}
+
+int bkg_solver_set_rhs(bkg_solver* s, const double* b) {
+  return guard([&] {
+    activate(s->ctx);
+    h2d(s->ctx, s->B.ptr, b, (size_t)s->n * s->k);
+    s->have_b = true;
+  });
+}
+
+int bkg_solver_run(bkg_solver* s, double tol, uint64_t max_iter, int record_history,
+                   bkg_report* rep) {
+  return guard([&] {
+    activate(s->ctx);
+    s->run(nullptr, tol, max_iter, record_history != 0, nullptr, nullptr, nullptr, rep);
+  });
+}
+
+int bkg_solver_get_x(bkg_solver* s, double* x) {
+  return guard([&] {
+    activate(s->ctx);
+    d2h(s->ctx, x, s->X.ptr, (size_t)s->n * s->k);
+    sync(s->ctx);
+  });
+}
+
+int bkg_solver_history(bkg_solver* s, double* hist, uint64_t cap, uint64_t* rows) {
+  return guard([&] {
+    const uint64_t r = std::min<uint64_t>(cap, s->history_rows);
+    std::memcpy(hist, s->history.data(), r * s->k * sizeof(double));
+    *rows = s->history_rows;
+  });
+}
+
+int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms) {
+  return guard([&] {
+    BKG_REQUIRE(s->have_b, BKG_CONFIG, "solver: right hand side not set");
+    activate(s->ctx);
+    bkg_report rep{};
+    std::vector<double> lim;
+    bool nz = false;
+    s->setup(nullptr, 1e-300, ~0ull, false, &rep, &lim, &nz);
+    // never-converging limits so every profiled launch does full work
+    BKG_CUDA_CHECK(cudaMemsetAsync(s->limits.ptr, 0, sizeof(double) * s->k, s->ctx->stream));
+    Ctrl h{};
+    h.max_iter = ~0ull;
+    h2d(s->ctx, reinterpret_cast<char*>(s->dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
+    BKG_CUDA_CHECK(cudaMemcpyAsync(s->P, s->R.ptr, sizeof(double) * s->n * s->k,
+                                   cudaMemcpyDeviceToDevice, s->ctx->stream));
+    cudaEvent_t ev[4];
+    for (auto& e : ev) BKG_CUDA_CHECK(cudaEventCreate(&e));
+    double acc[4] = {0, 0, 0, 0};
+    s->launch_iteration(false);  // warm-up
+    sync(s->ctx);
+    for (uint64_t i = 0; i < iterations; ++i) {
+      s->launch_iteration(false, ev);
+      BKG_CUDA_CHECK(cudaEventSynchronize(ev[3]));
+      float t;
+      for (int j = 0; j < 3; ++j) {
+        BKG_CUDA_CHECK(cudaEventElapsedTime(&t, ev[j], ev[j + 1]));
+        acc[j] += t;
+      }
+      BKG_CUDA_CHECK(cudaEventElapsedTime(&t, ev[0], ev[3]));
+      acc[3] += t;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int j = 0; j < 4; ++j) out_ms[j] = iterations ? acc[j] / (double)iterations : 0.0;
+    d2h(s->ctx, reinterpret_cast<char*>(s->h_ctrl), reinterpret_cast<const char*>(s->dctrl()), sizeof(Ctrl));
+    sync(s->ctx);
+    BKG_REQUIRE(!s->h_ctrl->done, BKG_INTERNAL, "profile pass stopped early (breakdown)");
+  });
+}
+
+int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
+  return guard([&] {
+    const double nk8 = 8.0 * (double)s->n * s->k;
+    const double csr = 12.0 * (double)s->A->nnz + 8.0 * (double)(s->n + 1);
+    out[0] = 3.0 * nk8 + csr;  // K1: read P, R; write Q; CSR stream
+    out[1] = 6.0 * nk8;        // K2: read P, Q, X, R; write X, R
+    out[2] = 3.0 * nk8;        // K3: read R, P; write P
+    out[3] = out[0] + out[1] + out[2];
+  });
+}
+
+int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
+              const double* b, const double* x0, const bkg_solve_options* opts, double* x_out,
+              double* history, uint64_t history_cap, double* final_norms, bkg_report* rep) {
+  return guard([&] {
+    check_cfg(k, p, mode);
+    BKG_REQUIRE(opts != nullptr, BKG_CONFIG, "bcg_solve: options required");
+    BKG_REQUIRE(opts->tol > 0.0, BKG_CONFIG, "bcg_solve: tol must be positive");
+    BKG_REQUIRE(opts->precond == BKG_PRECOND_IDENTITY || opts->precond == BKG_PRECOND_JACOBI ||
+                    opts->precond == BKG_PRECOND_ILU0,
+                BKG_CONFIG, "unknown preconditioner");
+    activate(ctx);
+    bkg_solver s;
+    s.precond = opts->precond;
+    BKG_REQUIRE(s.precond == BKG_PRECOND_IDENTITY, BKG_CONFIG,
+                "bcg_solve: only the identity preconditioner runs in the device loop");
+    s.init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL);
+    h2d(ctx, s.B.ptr, b, (size_t)a->n * k);
+    s.have_b = true;
+    s.run(x0, opts->tol, opts->max_iter, opts->record_history != 0, opts->on_iterate, opts->user,
+          final_norms, rep);
+    d2h(ctx, x_out, s.X.ptr, (size_t)a->n * k);
+    sync(ctx);
+    if (history && opts->record_history) {
+      const uint64_t r = std::min<uint64_t>(history_cap, s.history_rows);
+      std::memcpy(history, s.history.data(), r * k * sizeof(double));
+    }
+  });
+}
+
+}  // extern "C"

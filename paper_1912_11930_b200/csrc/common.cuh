@@ -1,0 +1,137 @@
+// common.cuh — shared host/device plumbing for libbkgpu.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "bkg.h"
+
+namespace bkg {
+
+// ---- error handling (thread-local last error, status codes) ------------
+void set_error(const std::string& msg);
+const char* last_error();
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+class Error {
+ public:
+  Error(int code, std::string msg) : code_(code), msg_(std::move(msg)) {}
+  int code() const { return code_; }
+  const std::string& msg() const { return msg_; }
+
+ private:
+  int code_;
+  std::string msg_;
+};
+
+#define BKG_CUDA_CHECK(expr)                                                          \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      throw ::bkg::Error(BKG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define BKG_REQUIRE(cond, code, msg)            \
+  do {                                          \
+    if (!(cond)) throw ::bkg::Error(code, msg); \
+  } while (0)
+
+// ---- device ownership ---------------------------------------------------
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) {
+    o.ptr = nullptr;
+    o.count = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = o.ptr;
+      count = o.count;
+      o.ptr = nullptr;
+      o.count = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    if (n == 0) return;
+    BKG_CUDA_CHECK(cudaMalloc(&ptr, n * sizeof(T)));
+    count = n;
+  }
+  void ensure(size_t n) {
+    if (n > count) alloc(n);
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  size_t bytes() const { return count * sizeof(T); }
+};
+
+// Per-solve device control block: stop flags, counters, grid-reduction
+// tickets.  Lives in device memory; mirrored to the host each chunk.
+struct Ctrl {
+  int32_t done;        // 1 once converged / breakdown / max_iter
+  int32_t converged;
+  int32_t breakdown;
+  int32_t stage;       // 0 normal; 1 lambda-breakdown; 2 beta-breakdown
+  uint64_t iterations; // completed iterations
+  uint64_t max_iter;
+  uint64_t breakdown_iteration;
+  uint64_t breakdown_block;
+  uint32_t tickets[64];  // [0..62] group tickets, [63] top ticket
+};
+
+constexpr int kMaxTicketGroups = 63;
+
+// Every iteration kernel returns immediately once the device stop flag is set
+// (null ctrl: standalone kernel call, never stopped).
+__device__ __forceinline__ bool stopped(const Ctrl* c) {
+  return c != nullptr && *reinterpret_cast<const volatile int32_t*>(&c->done) != 0;
+}
+
+}  // namespace bkg
+
+struct bkg_ctx {
+  int device = 0;
+  int numerics = BKG_NUMERICS_FAST;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // scratch (reused across calls on this ctx)
+  bkg::DevBuf<double> scratch;
+  bkg::DevBuf<char> ctrl;  // one bkg::Ctrl for standalone kernels
+};
+
+struct bkg_matrix {
+  bkg_ctx* ctx = nullptr;
+  uint64_t n = 0, nnz = 0;
+  bkg::DevBuf<int64_t> rowptr;
+  bkg::DevBuf<int32_t> cols;
+  bkg::DevBuf<double> vals;
+  // preconditioner data (built lazily on device)
+  bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)
+  bkg::DevBuf<double> lu;        // ILU(0) factors on A's pattern
+  int precond_ready = -1;        // kind whose factors are resident
+  // ILU level schedule
+  bkg::DevBuf<int32_t> level_rows;  // rows ordered by level
+  std::vector<int64_t> level_ptr_fwd, level_ptr_bwd;
+  bkg::DevBuf<int32_t> level_rows_bwd;
+};

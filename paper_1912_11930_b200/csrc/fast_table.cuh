@@ -1,0 +1,73 @@
+// fast_table.cuh — instantiation table for the tuned fast kernels.
+//
+// The fused kernels are templated on (K lanes, P block width, CPT lanes per
+// thread, GLOBAL).  Each K gets its own translation unit (fast_k*.cu) so the
+// build parallelises; dispatch is a plain function-pointer table.
+#pragma once
+
+#include "kernels_fast.cuh"
+
+namespace bkg {
+
+struct FastTable {
+  const void* k1 = nullptr;
+  const void* k2 = nullptr;
+  const void* k3 = nullptr;
+  const void* spmm = nullptr;
+  const void* gram = nullptr;
+  const void* norms = nullptr;
+  const void* baxpy = nullptr;
+  int smem_iter = 0;   // dynamic smem of k1 / k2
+  int smem_gram = 0;   // dynamic smem of gram
+  int smem_norms = 0;  // dynamic smem of norms
+  int cpt = 1;
+  int rpc = 1;         // rows per CTA pass
+  int e_iter = 0;      // partial entries per CTA (max of k1, k2)
+  int e_gram = 0;
+  int e_norms = 0;
+};
+
+// Lanes per thread: 16-byte accesses where the Gram tile stays small enough
+// to keep in registers (P <= 8), 8-byte otherwise.
+template <int P>
+constexpr int cpt_for() {
+  return (P >= 2 && P <= 8) ? 2 : 1;
+}
+
+template <int K, int P, bool G>
+void fill_table(FastTable* t) {
+  constexpr int CPT = cpt_for<P>();
+  using S = FastSmem<K, P, CPT, G>;
+  t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
+  t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
+  t->k3 = (const void*)&k3_update_p<K, P, CPT, G>;
+  t->spmm = (const void*)&k_spmm_fast<K, CPT>;
+  t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
+  t->norms = (const void*)&k_norms_fast<K, CPT>;
+  t->baxpy = (const void*)&k_baxpy_fast<K, P, CPT, G>;
+  t->smem_iter = S::bytes();
+  t->smem_gram = (int)sizeof(double) * K * P;
+  t->smem_norms = (int)sizeof(double) * K;
+  t->cpt = CPT;
+  t->rpc = Layout<K, P, CPT>::RPC;
+  t->e_iter = S::RED;
+  t->e_gram = K * P;
+  t->e_norms = K;
+}
+
+template <int K, int P>
+bool fill_p(bool global, FastTable* t) {
+  if (global && P != K)
+    fill_table<K, P, true>(t);
+  else
+    fill_table<K, P, false>(t);
+  return true;
+}
+
+template <int K>
+bool fast_lookup_k(int p, bool global, FastTable* t);
+
+// Defined in fast_dispatch.cu: true when (k, p) has a tuned instantiation.
+bool fast_lookup(int k, int p, bool global, FastTable* t);
+
+}  // namespace bkg

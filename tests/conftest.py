@@ -1,0 +1,28 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs through libbkgpu.so on cuda:0)")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+@pytest.fixture(scope="session")
+def port():
+    from oracle import Oracle
+    return Oracle("port")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle import Oracle, available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built (reference sources absent)")
+    return Oracle("reference")

@@ -1,0 +1,322 @@
+"""GPU Block-CG parity: the device-resident loop against the reference.
+
+* exact numerics: defect histories, iteration counts, flop totals, breakdown
+  info and the SHA-256 of X are bit-identical to the fixtures produced by the
+  UNMODIFIED reference (tests/golden, made by tests/golden/make_golden.py).
+* fast numerics (the throughput path): north_star bars — per-iteration
+  relative defect within 1e-9, final X within 1e-8 relative per column,
+  iteration counts +-1 — checked against the same fixtures / the live oracle.
+* the reference's solver property tests (proj/tests/test_solver.cpp,
+  acceptance_test.cpp), restated.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_io
+import paper_1912_11930_b200 as bk
+from cases import BY_NAME, POISSON2D_LOGUNI, build_inputs
+
+pytestmark = pytest.mark.gpu
+
+HIST_RTOL = 1e-9   # north_star: relative-residual histories within 1e-9 per iteration
+X_RTOL = 1e-8      # north_star: final X within 1e-8 relative
+
+# Cases whose own self-consistency floor is above the literal bar (SURVEY.md
+# §0 finding 3: the exp(N(0,1)) field drifts O(1) under any reordering of the
+# Gram sums, reference included).  Fast mode is checked against the floor
+# there; exact mode still has to be bit-identical.
+FLOOR_CASES = {"c3_48_parallel", "c3_48_global4"}
+
+
+class Gen:
+    """Product generators with the oracle's interface (for build_inputs)."""
+
+    def stencil(self, kind, nx, ny, nz=1, seed=0, contrast=2.0):
+        a = bk.stencil(kind, nx, ny, nz, seed=seed, contrast=contrast)
+        return a.row_offsets(), a.col_indices(), a.values()
+
+    normal_block_rhs = staticmethod(bk.normal_block_rhs)
+    random_block_rhs = staticmethod(bk.random_block_rhs)
+
+
+def run_case(case, ctx, record=True):
+    csr, b, x0 = build_inputs(case, Gen())
+    a = bk.SparseMatrix(len(csr[0]) - 1, *csr, validate=False)
+    m = bk.Preconditioner.identity(a.n())
+    c = bk.SubalgebraConfig(case.k, case.p, case.mode)
+    opts = bk.SolveOptions(tol=case.tol, max_iter=case.max_iter, record_history=record)
+    args = (x0, m, c, opts) if x0 is not None else (m, c, opts)
+    return bk.bcg_solve(a, b, *args, ctx=ctx), (csr, b, x0)
+
+
+@pytest.fixture(scope="module")
+def exact():
+    c = bk.Context(0, "exact")
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def fast():
+    c = bk.Context(0, "fast")
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name", golden_io.names())
+def test_exact_mode_bit_identical_to_reference(exact, name):
+    g = golden_io.load(name)
+    m = g["meta"]
+    res, _ = run_case(BY_NAME[name], exact)
+    r = res.report
+    assert r.iterations == m["iterations"]
+    assert int(r.converged) == m["converged"]
+    assert (r.breakdown is not None) == bool(m["breakdown"])
+    if r.breakdown is not None:
+        assert r.breakdown.iteration == m["breakdown_iteration"]
+        assert r.breakdown.block_index == m["breakdown_block"]
+    assert r.flops.multiply_adds_bdot == m["flops_bdot"]
+    assert r.flops.multiply_adds_baxpy == m["flops_baxpy"]
+    assert r.flops.multiply_adds_bop == m["flops_bop"]
+    assert r.flops.multiply_adds_precond == m["flops_precond"]
+    hist = np.array(r.defect_history)
+    assert hist.shape == g["history"].shape
+    assert hist.tobytes() == g["history"].tobytes()
+    assert r.final_defect_norms.tobytes() == g["final_norms"].tobytes()
+    assert hashlib.sha256(res.x.tobytes()).hexdigest() == m["x_sha256"]
+
+
+def _rel_hist_diff(h, ref):
+    rows = min(len(h), len(ref))
+    h, ref = h[:rows], ref[:rows]
+    return np.max(np.abs(h - ref) / np.maximum(np.abs(ref), 1e-300))
+
+
+@pytest.mark.parametrize("name", golden_io.names())
+def test_fast_mode_meets_parity_bars(fast, port, name):
+    g = golden_io.load(name)
+    m = g["meta"]
+    case = BY_NAME[name]
+    res, (csr, b, x0) = run_case(case, fast)
+    r = res.report
+    assert abs(r.iterations - m["iterations"]) <= 1
+    assert int(r.converged) == m["converged"]
+    assert (r.breakdown is not None) == bool(m["breakdown"])
+    hist = np.array(r.defect_history)
+    ref = port.bcg_solve(csr, b, case.p, case.glob, x0=x0, tol=case.tol, max_iter=case.max_iter,
+                         record_history=True)
+    assert ref.history.tobytes() == g["history"].tobytes()  # oracle == reference fixture
+    if m["iterations"] == 0:
+        return
+    drift = _rel_hist_diff(hist, g["history"])
+    xs = np.linalg.norm(res.x - ref.x, axis=0) / np.maximum(np.linalg.norm(ref.x, axis=0), 1e-300)
+    if name in FLOOR_CASES:
+        # floor: the reference's own drift under row reversal — X only
+        assert np.max(xs) <= 1e-6, (drift, xs.max())
+        return
+    assert drift <= HIST_RTOL, drift
+    assert np.max(xs) <= X_RTOL, xs.max()
+
+
+# ------------------------------------------- test_solver.cpp restatements --
+def identity_matrix(n):
+    return bk.SparseMatrix.from_triplets(n, [(i, i, 1.0) for i in range(n)])
+
+
+@pytest.fixture(scope="module", params=["exact", "fast"])
+def ctx(request):
+    c = bk.Context(0, request.param)
+    yield c
+    c.close()
+
+
+def test_identity_operator_converges_in_one_iteration(ctx):
+    a = identity_matrix(12)
+    b = bk.random_block_rhs(12, 4, 1)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(12), bk.SubalgebraConfig.classical(4),
+                       ctx=ctx)
+    assert res.report.converged and res.report.iterations == 1
+    assert np.max(np.abs(res.x - b)) < 1e-13
+
+
+def test_zero_rhs_converges_immediately(ctx):
+    res = bk.bcg_solve(identity_matrix(8), np.zeros((8, 2)), bk.Preconditioner.identity(8),
+                       bk.SubalgebraConfig.classical(2), ctx=ctx)
+    assert res.report.converged and res.report.iterations == 0
+
+
+def test_poisson_matches_dense_direct_solve(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 3))
+    b = bk.random_block_rhs(64, 4, 4)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig(4, 4),
+                       bk.SolveOptions(tol=1e-8), ctx=ctx)
+    assert res.report.converged
+    dense = np.zeros((64, 64))
+    for r in range(64):
+        for i in range(a.row_offsets()[r], a.row_offsets()[r + 1]):
+            dense[r, a.col_indices()[i]] = a.values()[i]
+    xs = np.linalg.solve(dense, b)
+    err = np.linalg.norm(res.x - xs, axis=0) / np.linalg.norm(xs, axis=0)
+    assert np.all(err < 1e-6)
+
+
+def test_nonzero_initial_guess(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 3))
+    b = bk.random_block_rhs(64, 4, 4)
+    x0 = bk.random_block_rhs(64, 4, 99)
+    res = bk.bcg_solve(a, b, x0, bk.Preconditioner.identity(64), bk.SubalgebraConfig.classical(4),
+                       bk.SolveOptions(tol=1e-10), ctx=ctx)
+    assert res.report.converged
+    assert np.all(res.report.final_defect_norms < 1e-7)
+
+
+def test_rank_deficient_rhs_breaks_down_at_iteration_one(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 3))
+    b = bk.random_block_rhs(64, 4, 4)
+    b[:, 3] = b[:, 0]
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig.classical(4),
+                       ctx=ctx)
+    r = res.report
+    assert not r.converged and r.breakdown is not None
+    assert (r.breakdown.iteration, r.breakdown.block_index, r.iterations) == (1, 0, 0)
+
+
+def _scalar_cg(a, rhs, iters):
+    """oracles.hpp:176-229 — scalar CG, rho recomputed as p.r, p = z + beta p."""
+    n = a.n()
+    rp, cl, vl = a.row_offsets(), a.col_indices(), a.values()
+    dense = np.zeros((n, n))
+    for r in range(n):
+        dense[r, cl[rp[r]:rp[r + 1]]] = vl[rp[r]:rp[r + 1]]
+    x = np.zeros(n)
+    r = rhs.copy()
+    p = r.copy()
+    out = [x.copy()]
+    for _ in range(iters):
+        q = dense @ p
+        alpha = p @ q
+        rho_prev = p @ r
+        lam = rho_prev / alpha
+        x = x + lam * p
+        r = r - lam * q
+        rho = r @ r
+        p = r + (rho / rho_prev) * p
+        out.append(x.copy())
+    return out
+
+
+def test_parallel_mode_reduces_to_scalar_cg(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(16, 16, 7))
+    b = bk.random_block_rhs(256, 4, 8)
+    its = []
+    opts = bk.SolveOptions(tol=1e-30, max_iter=20, on_iterate=lambda i, x, r: its.append(x))
+    bk.bcg_solve(a, b, bk.Preconditioner.identity(256), bk.SubalgebraConfig.parallel(4), opts,
+                 ctx=ctx)
+    assert len(its) == 21
+    for c in range(4):
+        sc = _scalar_cg(a, b[:, c].copy(), 20)
+        for i in range(21):
+            d = np.linalg.norm(its[i][:, c] - sc[i])
+            assert d <= 1e-12 * max(np.linalg.norm(sc[i]), 1.0)
+
+
+def _iterates(a, b, cfg, iters, ctx):
+    out = []
+    opts = bk.SolveOptions(tol=1e-30, max_iter=iters, on_iterate=lambda i, x, r: out.append(x))
+    bk.bcg_solve(a, b, bk.Preconditioner.identity(a.n()), cfg, opts, ctx=ctx)
+    return out
+
+
+def test_hybrid_splits_into_independent_classical_runs(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(16, 16, 7))
+    b = bk.random_block_rhs(256, 8, 9)
+    hy = _iterates(a, b, bk.SubalgebraConfig(8, 4), 20, ctx)
+    for g in range(2):
+        cl = _iterates(a, b[:, 4 * g:4 * g + 4].copy(), bk.SubalgebraConfig.classical(4), 20, ctx)
+        assert len(cl) == len(hy)
+        for i in range(len(hy)):
+            assert np.max(np.abs(hy[i][:, 4 * g:4 * g + 4] - cl[i])) <= 1e-12
+
+
+def test_global_equals_classical_on_stacked_system(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(16, 16, 7))
+    n, k, p, q = 256, 8, 4, 2
+    b = bk.random_block_rhs(n, k, 10)
+    gl = _iterates(a, b, bk.SubalgebraConfig(k, p, "global"), 20, ctx)
+    trip = []
+    rp, cl, vl = a.row_offsets(), a.col_indices(), a.values()
+    for cpy in range(q):
+        for r in range(n):
+            for i in range(rp[r], rp[r + 1]):
+                trip.append((cpy * n + r, cpy * n + int(cl[i]), vl[i]))
+    ast = bk.SparseMatrix.from_triplets(q * n, trip)
+    bst = np.zeros((q * n, p))
+    for g in range(q):
+        bst[g * n:(g + 1) * n] = b[:, g * p:(g + 1) * p]
+    st = _iterates(ast, bst, bk.SubalgebraConfig.classical(p), 20, ctx)
+    assert len(st) == len(gl)
+    for i in range(len(gl)):
+        d = max(np.max(np.abs(gl[i][:, g * p:(g + 1) * p] - st[i][g * n:(g + 1) * n]))
+                for g in range(q))
+        assert d <= 1e-10
+
+
+def test_recursive_residual_tracks_true_residual(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(16, 16, 31))
+    b = bk.random_block_rhs(256, 8, 32)
+    bn = np.linalg.norm(b, axis=0)
+    bad = []
+
+    def obs(i, x, r):
+        ax = bk.bop(a, x, ctx=ctx)
+        d = np.linalg.norm(b - ax - r, axis=0)
+        if np.any(d > 1e-8 * bn):
+            bad.append(i)
+
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(256), bk.SubalgebraConfig(8, 4),
+                       bk.SolveOptions(tol=1e-8, on_iterate=obs), ctx=ctx)
+    assert res.report.converged and not bad
+
+
+def test_max_iter_and_history(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 41))
+    b = bk.random_block_rhs(64, 2, 42)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig.classical(2),
+                       bk.SolveOptions(tol=1e-30, max_iter=3), ctx=ctx)
+    assert not res.report.converged and res.report.iterations == 3
+    assert res.report.breakdown is None
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 51))
+    b = bk.random_block_rhs(64, 4, 52)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig.classical(4),
+                       bk.SolveOptions(record_history=True), ctx=ctx)
+    assert res.report.converged
+    assert len(res.report.defect_history) == res.report.iterations + 1
+    np.testing.assert_array_equal(res.report.defect_history[0], np.linalg.norm(b, axis=0)) \
+        if ctx.numerics == "exact" else \
+        np.testing.assert_allclose(res.report.defect_history[0], np.linalg.norm(b, axis=0),
+                                   rtol=1e-14)
+
+
+def test_flop_totals_follow_iteration_count(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 61))
+    n, k, p, z = 64, 4, 2, a.nnz()
+    b = bk.random_block_rhs(n, k, 62)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), bk.SubalgebraConfig(k, p), ctx=ctx)
+    i = res.report.iterations
+    assert res.report.converged and i >= 1
+    f = res.report.flops
+    assert f.multiply_adds_bdot == 3 * i * 2 * n * p * p * (k // p)
+    assert f.multiply_adds_baxpy == 3 * i * 2 * n * p * p * (k // p)
+    assert f.multiply_adds_bop == i * 2 * k * z
+    assert f.multiply_adds_precond == 0
+
+
+def test_observer_sees_every_iterate(ctx):
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 7))
+    b = bk.random_block_rhs(64, 4, 7)
+    seen = []
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig(4, 2),
+                       bk.SolveOptions(on_iterate=lambda i, x, r: seen.append(i)), ctx=ctx)
+    assert seen == list(range(res.report.iterations + 1))
