@@ -23,11 +23,6 @@ pytestmark = pytest.mark.gpu
 HIST_RTOL = 1e-9   # north_star: relative-residual histories within 1e-9 per iteration
 X_RTOL = 1e-8      # north_star: final X within 1e-8 relative
 
-# Cases whose own self-consistency floor is above the literal bar (SURVEY.md
-# §0 finding 3: the exp(N(0,1)) field drifts O(1) under any reordering of the
-# Gram sums, reference included).  Fast mode is checked against the floor
-# there; exact mode still has to be bit-identical.
-FLOOR_CASES = {"c3_48_parallel", "c3_48_global4"}
 
 
 class Gen:
@@ -101,23 +96,25 @@ def test_fast_mode_meets_parity_bars(fast, port, name):
     case = BY_NAME[name]
     res, (csr, b, x0) = run_case(case, fast)
     r = res.report
-    assert abs(r.iterations - m["iterations"]) <= 1
     assert int(r.converged) == m["converged"]
     assert (r.breakdown is not None) == bool(m["breakdown"])
     hist = np.array(r.defect_history)
     ref = port.bcg_solve(csr, b, case.p, case.glob, x0=x0, tol=case.tol, max_iter=case.max_iter,
                          record_history=True)
     assert ref.history.tobytes() == g["history"].tobytes()  # oracle == reference fixture
-    if m["iterations"] == 0:
-        return
-    drift = _rel_hist_diff(hist, g["history"])
+    drift = _rel_hist_diff(hist, g["history"]) if m["iterations"] else 0.0
     xs = np.linalg.norm(res.x - ref.x, axis=0) / np.maximum(np.linalg.norm(ref.x, axis=0), 1e-300)
-    if name in FLOOR_CASES:
-        # floor: the reference's own drift under row reversal — X only
-        assert np.max(xs) <= 1e-6, (drift, xs.max())
-        return
-    assert drift <= HIST_RTOL, drift
     assert np.max(xs) <= X_RTOL, xs.max()
+    if m["floor_hist_drift"] <= HIST_RTOL:
+        # the reference itself is reorder-stable here: literal north_star bars
+        assert abs(r.iterations - m["iterations"]) <= 1
+        assert drift <= HIST_RTOL, drift
+    else:
+        # floor case: the reference drifts O(1) per iteration under a mere row
+        # reversal (m["floor_hist_drift"]), so no reordered
+        # implementation can meet 1e-9; require the iteration count within 2%
+        # and the final X bar (exact mode is still bit-identical, above).
+        assert abs(r.iterations - m["iterations"]) <= max(1, int(0.02 * m["iterations"]))
 
 
 # ------------------------------------------- test_solver.cpp restatements --
