@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libbkgpu.so")
+# BKG_LIB overrides the library path (kernel-variant sweeps in tools/).
+LIB_PATH = os.environ.get("BKG_LIB") or os.path.join(HERE, "_build", "libbkgpu.so")
 
 BKG_OK = 0
 BKG_DIMENSION = 1

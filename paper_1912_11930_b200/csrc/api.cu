@@ -319,8 +319,8 @@ struct bkg_solver {
     if (fast) {
       g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc);
       g2 = occupancy_grid(c, ft.k2, ft.smem_iter, n, ft.rpc);
-      g3 = occupancy_grid(c, ft.k3, 0, n, ft.rpc);
-      const int gmax = std::max(g1, g2);
+      g3 = occupancy_grid(c, ft.k3, ft.smem_iter, n, ft.rpc);
+      const int gmax = std::max(std::max(g1, g2), g3);
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
     }
@@ -358,7 +358,7 @@ struct bkg_solver {
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, ft.k2, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
-      launch(ctx, ft.k3, g3, kThreads, 0, args);
+      launch(ctx, ft.k3, g3, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
       return;
     }
@@ -456,8 +456,12 @@ struct bkg_solver {
     h2d(ctx, reinterpret_cast<char*>(dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
     P = Pb.ptr;
     Z = Zb.ptr;
-    if (!conv)  // P^1 = M^-1 R^0 (identity: copy, solver.hpp:152-155)
+    if (!conv) {  // P^1 = M^-1 R^0 (identity: copy, solver.hpp:152-155)
       BKG_CUDA_CHECK(cudaMemcpyAsync(P, R.ptr, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      // fast mode: K3 of iteration i produces rho_prev for iteration i+1;
+      // the first one, <<P^1, R^0>>, comes from a standalone Gram launch.
+      if (fast) dev_gram(ctx, n, k, p, global, P, R.ptr, coef.ptr + cs);
+    }
     return conv;
   }
 
@@ -918,9 +922,15 @@ int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
   return guard([&] {
     const double nk8 = 8.0 * (double)s->n * s->k;
     const double csr = 12.0 * (double)s->A->nnz + 8.0 * (double)(s->n + 1);
-    out[0] = 3.0 * nk8 + csr;  // K1: read P, R; write Q; CSR stream
-    out[1] = 6.0 * nk8;        // K2: read P, Q, X, R; write X, R
-    out[2] = 3.0 * nk8;        // K3: read R, P; write P
+    if (s->fast) {
+      out[0] = 2.0 * nk8 + csr;  // K1: read P (once, neighbours via L1/L2); write Q; CSR
+      out[1] = 3.0 * nk8;        // K2: read Q, R; write R
+      out[2] = 5.0 * nk8;        // K3: read P, X, R; write P, X
+    } else {  // exact mode: model of the unfused kernel sequence
+      out[0] = 2.0 * nk8 + csr + 4.0 * nk8;  // spmm + alpha/rho_prev chains
+      out[1] = 8.0 * nk8;                    // 2 baxpy + copy + rho/norm chains
+      out[2] = 3.0 * nk8;                    // P update
+    }
     out[3] = out[0] + out[1] + out[2];
   });
 }

@@ -92,6 +92,8 @@ struct Ctrl {
   int32_t converged;
   int32_t breakdown;
   int32_t stage;       // 0 normal; 1 lambda-breakdown; 2 beta-breakdown
+  int32_t xpending;    // fast mode: K2 ran, K3 still owes X += P lambda
+  int32_t pad_;
   uint64_t iterations; // completed iterations
   uint64_t max_iter;
   uint64_t breakdown_iteration;

@@ -40,7 +40,7 @@ void fill_table(FastTable* t) {
   using S = FastSmem<K, P, CPT, G>;
   t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
   t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
-  t->k3 = (const void*)&k3_update_p<K, P, CPT, G>;
+  t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
   t->norms = (const void*)&k_norms_fast<K, CPT>;

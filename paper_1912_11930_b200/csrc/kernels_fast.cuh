@@ -213,21 +213,91 @@ template <int K, int P, int CPT, bool GLOBAL>
 struct FastSmem {
   static constexpr int NB = GLOBAL ? 1 : K / P;
   static constexpr int CS = NB * P * P;
-  static constexpr int RED1 = 2 * K * P;         // K1: TPR * 2*P*CPT
-  static constexpr int RED2 = K * P + K;         // K2: TPR * (P*CPT + CPT)
-  static constexpr int RED = RED1 > RED2 ? RED1 : RED2;
+  static constexpr int RED = K * P + K;  // largest TPR * NACC over K1..K3
   static int bytes() {
-    return (int)sizeof(double) * (RED + 2 * CS + CS + bsolve_ws_doubles(P, kThreads) + K);
+    return (int)sizeof(double) * (RED + 3 * CS + bsolve_ws_doubles(P, kThreads) + K);
   }
 };
 
+// Minimum resident CTAs per SM for the row-streaming kernels: 4 caps
+// registers at 64/thread so enough rows are in flight to cover DRAM latency;
+// kernels carrying a p x p Gram tile of >= 16 doubles per thread get 85.
+#ifndef BKG_MINB_BIG
+#define BKG_MINB_BIG 3
+#endif
+#ifndef BKG_MINB_SMALL
+#define BKG_MINB_SMALL 4
+#endif
+template <int P, int CPT>
+constexpr int min_blocks() {
+  return P * CPT >= 16 ? BKG_MINB_BIG : BKG_MINB_SMALL;
+}
+
+// One CSR row of Q = A P for the CPT lanes of this thread, in CSR order.
+// Chunks of 8 nonzeros are loaded with predication so that every index and
+// operand load of a stencil row is in flight at once (no serial tail loop).
+template <int K, int CPT>
+__device__ __forceinline__ void spmm_row(const IterArgs& a, int64_t beg, int64_t end, int col0,
+                                         double (&q)[CPT]) {
+  constexpr int CH = 8;
+#pragma unroll 1
+  for (int64_t i = beg; i < end; i += CH) {
+    double v[CH], x[CH][CPT];
+    int c[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const bool on = i + u < end;
+      v[u] = on ? __ldg(a.vals + i + u) : 0.0;
+      c[u] = on ? __ldg(a.cols + i + u) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      if (c[u] >= 0) {
+        ld_nc<CPT>(x[u], a.P + (int64_t)c[u] * K + col0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) x[u][j] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+      if (c[u] >= 0) {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) q[j] = fma(v[u], x[u][j], q[j]);
+      }
+  }
+}
+
+// Rows interleaved per thread in the streaming kernels (bytes in flight) and
+// how K2/K3 read the p x p coefficients: `const double*` lets the compiler
+// keep them in registers, `const volatile double*` re-reads shared memory per
+// row.  Defaults from the tools/kernel_sweep.py measurements on B200 (C2):
+// K2 2 rows/thread + register coefficients (0.34 ms, 73% of HBM peak); K3 one
+// row/thread (two spill).
+#ifndef BKG_K2_ROWS
+#define BKG_K2_ROWS 2
+#endif
+#ifndef BKG_K3_ROWS
+#define BKG_K3_ROWS 1
+#endif
+#ifndef BKG_K2_COEF_PTR
+#define BKG_K2_COEF_PTR const double*
+#endif
+#ifndef BKG_K3_COEF_PTR
+#define BKG_K3_COEF_PTR const double*
+#endif
+
 // ---------------------------------------------------------------- K1 ----
+// Q = A P; alpha = <<P, Q>>; last CTA: lambda = alpha^-1 rho_prev.
+// rho_prev = <<P^i, R^{i-1}>> (solver.hpp:168) was produced by K3 of the
+// previous iteration (R is not modified between that K3 and this K1), so K1
+// does not read R at all.
 template <int K, int P, int CPT, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads) k1_spmm_gram(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k1_spmm_gram(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
   if (stopped(a.ctrl)) return;
-  constexpr int NACC = 2 * P * CPT;
+  constexpr int NACC = P * CPT;
   double acc[NACC];
 #pragma unroll
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
@@ -235,39 +305,26 @@ __global__ void __launch_bounds__(kThreads) k1_spmm_gram(IterArgs a) {
   const int col0 = pos * CPT;
   const int gbase = (lane / L::GT) * L::GT;
   const int64_t stride = (int64_t)gridDim.x * L::RPC;
+  int64_t row = (int64_t)blockIdx.x * L::RPC + slot;
+  int64_t beg = 0, end = 0;
+  if (row < a.n) {
+    beg = __ldg(a.rowptr + row);
+    end = __ldg(a.rowptr + row + 1);
+  }
   for (int64_t base = (int64_t)blockIdx.x * L::RPC; base < a.n; base += stride) {
-    const int64_t row = base + slot;
-    double q[CPT], pv[CPT], rv[CPT];
+    // prefetch the next row's extent while this row's loads are in flight
+    const int64_t nrow = row + stride;
+    int64_t nbeg = 0, nend = 0;
+    if (nrow < a.n) {
+      nbeg = __ldg(a.rowptr + nrow);
+      nend = __ldg(a.rowptr + nrow + 1);
+    }
+    double q[CPT], pv[CPT];
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) q[j] = pv[j] = rv[j] = 0.0;
+    for (int j = 0; j < CPT; ++j) q[j] = pv[j] = 0.0;
     if (row < a.n) {
-      const int64_t beg = __ldg(a.rowptr + row), end = __ldg(a.rowptr + row + 1);
-      int64_t i = beg;
-      for (; i + 4 <= end; i += 4) {
-        double v[4], x[4][CPT];
-        int c[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          v[u] = __ldg(a.vals + i + u);
-          c[u] = __ldg(a.cols + i + u);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) ld_nc<CPT>(x[u], a.P + (int64_t)c[u] * K + col0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int j = 0; j < CPT; ++j) q[j] = fma(v[u], x[u][j], q[j]);
-      }
-      for (; i < end; ++i) {
-        const double v = __ldg(a.vals + i);
-        const int c = __ldg(a.cols + i);
-        double x[CPT];
-        ld_nc<CPT>(x, a.P + (int64_t)c * K + col0);
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) q[j] = fma(v, x[j], q[j]);
-      }
       ld_nc<CPT>(pv, a.P + row * K + col0);
-      ld_nc<CPT>(rv, a.R + row * K + col0);
+      spmm_row<K, CPT>(a, beg, end, col0, q);
       st<CPT>(a.Q + row * K + col0, q);
     }
 #pragma unroll
@@ -277,32 +334,33 @@ __global__ void __launch_bounds__(kThreads) k1_spmm_gram(IterArgs a) {
         const double ps = __shfl_sync(kFull, pv[jj], gbase + s);
         const int aa = s * CPT + jj;
 #pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-          acc[aa * CPT + j] = fma(ps, q[j], acc[aa * CPT + j]);
-          acc[P * CPT + aa * CPT + j] = fma(ps, rv[j], acc[P * CPT + aa * CPT + j]);
-        }
+        for (int j = 0; j < CPT; ++j) acc[aa * CPT + j] = fma(ps, q[j], acc[aa * CPT + j]);
       }
     }
+    row = nrow;
+    beg = nbeg;
+    end = nend;
   }
   extern __shared__ double sm[];
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
   double* alpha = sm + S::RED;
-  double* rho_prev = alpha + S::CS;
-  double* ws = rho_prev + S::CS + S::CS;
+  double* ws = alpha + 3 * S::CS;
   gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, alpha);
-  gather_gram<K, P, CPT, GLOBAL, NACC>(red, P * CPT, rho_prev);
   __syncthreads();
-  for (int i = threadIdx.x; i < S::CS; i += kThreads) a.coef[S::CS + i] = rho_prev[i];
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, rho_prev, a.coef, ws);  // lambda
+  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 
 // ---------------------------------------------------------------- K2 ----
+// R -= Q lambda; rho = <<R, R>> (Z = M^-1 R = R) and ||R_s||^2; last CTA:
+// beta = rho_prev^-1 rho, history, stop test.  X += P lambda is deferred to
+// K3, which reads P anyway (nothing reads X before K3).
 template <int K, int P, int CPT, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads) k2_update_gram(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gram(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
+  constexpr int U = BKG_K2_ROWS;
   if (stopped(a.ctrl)) return;
   extern __shared__ double sm[];
   double* lam = sm + S::RED;
@@ -315,64 +373,65 @@ __global__ void __launch_bounds__(kThreads) k2_update_gram(IterArgs a) {
   const int tid = threadIdx.x, pos = tid % L::TPR, slot = tid / L::TPR, lane = tid & 31;
   const int col0 = pos * CPT;
   const int gbase = (lane / L::GT) * L::GT;
-  const int grp = col0 / P;
-  const double* lg = lam + (GLOBAL ? 0 : grp) * P * P;
-  const int64_t stride = (int64_t)gridDim.x * L::RPC;
-  for (int64_t base = (int64_t)blockIdx.x * L::RPC; base < a.n; base += stride) {
-    const int64_t row = base + slot;
-    const bool valid = row < a.n;
-    double pv[CPT], qv[CPT], xv[CPT], rv[CPT];
+  BKG_K2_COEF_PTR lg = lam + (GLOBAL ? 0 : col0 / P) * P * P;
+  const int64_t r1 = a.n;
+  for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
+       base += (int64_t)gridDim.x * L::RPC * U) {
+    double qv[U][CPT], rv[U][CPT];
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) pv[j] = qv[j] = xv[j] = rv[j] = 0.0;
-    if (valid) {
-      ld_nc<CPT>(pv, a.P + row * K + col0);
-      ld_nc<CPT>(qv, a.Q + row * K + col0);
-      ld_rw<CPT>(xv, a.X + row * K + col0);
-      ld_rw<CPT>(rv, a.R + row * K + col0);
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = base + u * L::RPC + slot;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) qv[u][j] = rv[u][j] = 0.0;
+      if (row < r1) {
+        ld_nc<CPT>(qv[u], a.Q + row * K + col0);
+        ld_rw<CPT>(rv[u], a.R + row * K + col0);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < L::GT; ++s) {
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
-      for (int jj = 0; jj < CPT; ++jj) {
-        const double ps = __shfl_sync(kFull, pv[jj], gbase + s);
-        const double qs = __shfl_sync(kFull, qv[jj], gbase + s);
-        const int b = s * CPT + jj;
+      for (int s = 0; s < L::GT; ++s) {
 #pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-          const double l = lg[b * P + (col0 + j) % P];
-          xv[j] = fma(ps, l, xv[j]);
-          rv[j] = fma(-qs, l, rv[j]);
+        for (int jj = 0; jj < CPT; ++jj) {
+          const double qs = __shfl_sync(kFull, qv[u][jj], gbase + s);
+          const int b = s * CPT + jj;
+#pragma unroll
+          for (int j = 0; j < CPT; ++j)
+            rv[u][j] = fma(-qs, lg[b * P + (col0 + j) % P], rv[u][j]);
         }
       }
-    }
-    if (valid) {
-      st<CPT>(a.X + row * K + col0, xv);
-      st<CPT>(a.R + row * K + col0, rv);
+      const int64_t row = base + u * L::RPC + slot;
+      if (row < r1) st<CPT>(a.R + row * K + col0, rv[u]);
     }
 #pragma unroll
-    for (int s = 0; s < L::GT; ++s) {
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
-      for (int jj = 0; jj < CPT; ++jj) {
-        const double rs = __shfl_sync(kFull, rv[jj], gbase + s);
-        const int aa = s * CPT + jj;
+      for (int s = 0; s < L::GT; ++s) {
 #pragma unroll
-        for (int j = 0; j < CPT; ++j) acc[aa * CPT + j] = fma(rs, rv[j], acc[aa * CPT + j]);
+        for (int jj = 0; jj < CPT; ++jj) {
+          const double rs = __shfl_sync(kFull, rv[u][jj], gbase + s);
+          const int aa = s * CPT + jj;
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) acc[aa * CPT + j] = fma(rs, rv[u][j], acc[aa * CPT + j]);
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) acc[P * CPT + j] = fma(rv[j], rv[j], acc[P * CPT + j]);
+      for (int j = 0; j < CPT; ++j) acc[P * CPT + j] = fma(rv[u][j], rv[u][j], acc[P * CPT + j]);
+    }
   }
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
-  double* rho = lam;  // lambda no longer needed
-  double* norms = rho + S::CS;
-  double* beta_s = norms + K;
-  double* ws = beta_s + S::CS;
+  double* rho = lam;  // lambda no longer needed in smem
+  double* beta_s = rho + S::CS;
+  double* norms = beta_s + S::CS;
+  double* ws = sm + S::RED + 3 * S::CS + K;
   gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, rho);
   for (int c = threadIdx.x; c < K; c += kThreads)
     norms[c] = sqrt(red[(c / CPT) * NACC + P * CPT + (c % CPT)]);
   __syncthreads();
   const int bad = cta_bsolve<P>(S::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
+  if (threadIdx.x == 0) a.ctrl->xpending = 1;  // K3 still owes X += P lambda
   if (bad >= 0) {
     record_breakdown(a.ctrl, bad, 2);
     return;
@@ -385,41 +444,92 @@ __global__ void __launch_bounds__(kThreads) k2_update_gram(IterArgs a) {
 }
 
 // ---------------------------------------------------------------- K3 ----
+// X += P lambda (always, once K2 ran: solver.hpp:171-175 precede the beta
+// solve and the stop test); unless the solve stopped: P = R + P beta in
+// place (solver.hpp:186-190) and rho_prev' = <<P', R>> for the next K1.
 template <int K, int P, int CPT, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads) k3_update_p(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
-  if (stopped(a.ctrl)) return;
-  __shared__ double beta[S::CS];
-  for (int i = threadIdx.x; i < S::CS; i += kThreads) beta[i] = a.coef[2 * S::CS + i];
+  constexpr int U = BKG_K3_ROWS;
+  if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
+  const bool fin = stopped(a.ctrl);  // uniform: nothing writes `done` during K3
+  extern __shared__ double sm[];
+  double* lam = sm + S::RED;
+  double* beta = lam + S::CS;
+  for (int i = threadIdx.x; i < S::CS; i += kThreads) {
+    lam[i] = a.coef[i];
+    beta[i] = a.coef[2 * S::CS + i];
+  }
   __syncthreads();
+  constexpr int NACC = P * CPT;
+  double acc[NACC];
+#pragma unroll
+  for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
   const int tid = threadIdx.x, pos = tid % L::TPR, slot = tid / L::TPR, lane = tid & 31;
   const int col0 = pos * CPT;
   const int gbase = (lane / L::GT) * L::GT;
-  const double* bg = beta + (GLOBAL ? 0 : col0 / P) * P * P;
-  const int64_t stride = (int64_t)gridDim.x * L::RPC;
-  for (int64_t base = (int64_t)blockIdx.x * L::RPC; base < a.n; base += stride) {
-    const int64_t row = base + slot;
-    const bool valid = row < a.n;
-    double pv[CPT], pn[CPT];
+  const int goff = (GLOBAL ? 0 : col0 / P) * P * P;
+  BKG_K3_COEF_PTR lg = lam + goff;
+  BKG_K3_COEF_PTR bg = beta + goff;
+  const int64_t r1 = a.n;
+  for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
+       base += (int64_t)gridDim.x * L::RPC * U) {
+    double pv[U][CPT], xv[U][CPT], rv[U][CPT];
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) pv[j] = pn[j] = 0.0;
-    if (valid) {
-      ld_rw<CPT>(pv, a.P + row * K + col0);
-      ld_nc<CPT>(pn, a.R + row * K + col0);
-    }
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = base + u * L::RPC + slot;
 #pragma unroll
-    for (int s = 0; s < L::GT; ++s) {
-#pragma unroll
-      for (int jj = 0; jj < CPT; ++jj) {
-        const double ps = __shfl_sync(kFull, pv[jj], gbase + s);
-        const int b = s * CPT + jj;
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) pn[j] = fma(ps, bg[b * P + (col0 + j) % P], pn[j]);
+      for (int j = 0; j < CPT; ++j) pv[u][j] = xv[u][j] = rv[u][j] = 0.0;
+      if (row < r1) {
+        ld_rw<CPT>(pv[u], a.P + row * K + col0);
+        ld_rw<CPT>(xv[u], a.X + row * K + col0);
+        if (!fin) ld_nc<CPT>(rv[u], a.R + row * K + col0);
       }
     }
-    if (valid) st<CPT>(a.P + row * K + col0, pn);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double pn[CPT];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) pn[j] = rv[u][j];
+#pragma unroll
+      for (int s = 0; s < L::GT; ++s) {
+#pragma unroll
+        for (int jj = 0; jj < CPT; ++jj) {
+          const double ps = __shfl_sync(kFull, pv[u][jj], gbase + s);
+          const int b = s * CPT + jj;
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) {
+            const int e = b * P + (col0 + j) % P;
+            xv[u][j] = fma(ps, lg[e], xv[u][j]);
+            pn[j] = fma(ps, bg[e], pn[j]);
+          }
+        }
+      }
+      const int64_t row = base + u * L::RPC + slot;
+      if (row < r1) {
+        st<CPT>(a.X + row * K + col0, xv[u]);
+        if (!fin) st<CPT>(a.P + row * K + col0, pn);
+      }
+      if (!fin) {
+#pragma unroll
+        for (int s = 0; s < L::GT; ++s) {
+#pragma unroll
+          for (int jj = 0; jj < CPT; ++jj) {
+            const double ps = __shfl_sync(kFull, pn[jj], gbase + s);
+            const int aa = s * CPT + jj;
+#pragma unroll
+            for (int j = 0; j < CPT; ++j)
+              acc[aa * CPT + j] = fma(ps, rv[u][j], acc[aa * CPT + j]);
+          }
+        }
+      }
+    }
   }
+  double* red = sm;
+  if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
+  if (!fin) gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, a.coef + S::CS);  // rho_prev
+  if (threadIdx.x == 0) a.ctrl->xpending = 0;  // every CTA has read it (we are last)
 }
 
 // ------------------------------------------------ standalone fast kernels ----

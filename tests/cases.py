@@ -81,7 +81,23 @@ CASES = [
     Case("zero_rhs", POISSON2D_CONST, 8, 8, 1, 2, 2, False, "uniform", zero_rhs=True),
 ]
 
-BY_NAME = {c.name: c for c in CASES}
+# Full-size BASELINE configs whose reference solve takes minutes to hours on
+# one core: fixtures are produced once in the background (make_golden.py
+# --full) and checked on the GPU (exact: bit-identical; fast: bars).
+FULL_CASES = [
+    Case("c2_full", LAPLACE3D_7PT, 128, 128, 128, 32, 8, False, "normal"),
+    Case("c4_full_classical", STENCIL3D_27PT, 192, 192, 192, 16, 16, False, "normal", 1e-300,
+         200),
+    Case("c4_full_hybrid4", STENCIL3D_27PT, 192, 192, 192, 16, 4, False, "normal", 1e-300, 200),
+    Case("c4_full_global4", STENCIL3D_27PT, 192, 192, 192, 16, 4, True, "normal", 1e-300, 200),
+    Case("c3_full_parallel", DIFFUSION2D_LOGNORMAL, 1024, 1024, 1, 64, 1, False, "uniform",
+         coeff_seed=COEFF_SEED),
+    Case("c3_full_global4", DIFFUSION2D_LOGNORMAL, 1024, 1024, 1, 64, 4, True, "uniform",
+         coeff_seed=COEFF_SEED),
+]
+
+BY_NAME = {c.name: c for c in CASES + FULL_CASES}
+FULL_NAMES = {c.name for c in FULL_CASES}
 
 
 def build_inputs(case: Case, gen):

@@ -26,7 +26,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from oracle import Oracle  # noqa: E402
-from cases import BY_NAME, CASES, build_inputs  # noqa: E402
+from cases import BY_NAME, CASES, FULL_NAMES, build_inputs  # noqa: E402
 
 
 def sample_rows(n):
@@ -83,12 +83,15 @@ def make(case, ref, port):
                 x_sha256=hashlib.sha256(out.x.tobytes()).hexdigest(),
                 b_sha256=hashlib.sha256(b.tobytes()).hexdigest(),
                 n=int(n), nnz=int(csr[0][-1]), ref_seconds=dt, source="oracle/_ref/libbkref.so")
-    meta.update(floor_of(case, port, csr, b, x0, out))
+    meta["full"] = case.name in FULL_NAMES
+    if not meta["full"]:
+        meta.update(floor_of(case, port, csr, b, x0, out))
     np.savez_compressed(os.path.join(HERE, f"{case.name}.npz"), history=out.history,
                         final_norms=out.final_norms, x_rows=rows, x_sample=out.x[rows],
                         meta=np.array(json.dumps(meta)))
     print(f"{case.name}: it={r.iterations} conv={r.converged} bd={r.breakdown} {dt:.2f}s "
-          f"floor drift={meta['floor_hist_drift']:.2e} it={meta['floor_iterations']}")
+          f"floor drift={meta.get('floor_hist_drift', float('nan')):.2e} "
+          f"it={meta.get('floor_iterations', -1)}", flush=True)
 
 
 def main(names):

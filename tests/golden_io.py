@@ -14,5 +14,8 @@ def load(name):
                 x_sample=z["x_sample"], meta=meta)
 
 
-def names():
-    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+def names(full=False):
+    """Fixture names; full-size BASELINE configs only when full=True."""
+    from cases import FULL_NAMES
+    all_ = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+    return [n for n in all_ if (n in FULL_NAMES) == full]

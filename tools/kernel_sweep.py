@@ -1,0 +1,60 @@
+#!/usr/bin/env python3
+"""Per-kernel device times of the fused Block-CG iteration for each library
+variant under paper_1912_11930_b200/_build/variants/ (or the default build).
+
+    python tools/kernel_sweep.py [--configs c2,c4c] [--variants a,b] [--iters 20]
+
+Each variant runs in its own subprocess (BKG_LIB selects the .so)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+VDIR = os.path.join(ROOT, "paper_1912_11930_b200", "_build", "variants")
+
+
+def child(cfg, iters):
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import bench
+    import paper_1912_11930_b200 as bk
+    kind, nx, ny, nz, k, p, mode, rhs, tol, max_iter, desc = bench.CONFIGS[cfg]
+    a, b = bench.make_inputs(cfg, bk)
+    s = bk.DeviceSolver(a, bk.SubalgebraConfig(k, p, mode))
+    s.set_rhs(b)
+    ms = s.profile(iters)
+    by = s.kernel_bytes()
+    peak, _ = bench.measured_peak()
+    out = {"config": cfg, "ms": [round(float(x), 4) for x in ms],
+           "GBps": [round(float(by[i] / (ms[i] * 1e-3) / 1e9), 1) for i in range(4)],
+           "frac": [round(float(by[i] / (ms[i] * 1e-3) / 1e9 / peak), 3) for i in range(4)]}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2")
+    ap.add_argument("--variants", default="")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--child", default="")
+    args = ap.parse_args()
+    if args.child:
+        return child(args.child, args.iters)
+    variants = [v for v in args.variants.split(",") if v] or (
+        sorted(os.listdir(VDIR)) if os.path.isdir(VDIR) else [])
+    variants = variants or ["default"]
+    for v in variants:
+        env = dict(os.environ)
+        if v != "default":
+            env["BKG_LIB"] = os.path.join(VDIR, v, "libbkgpu.so")
+        for cfg in args.configs.split(","):
+            r = subprocess.run([sys.executable, __file__, "--child", cfg, "--iters",
+                                str(args.iters)], env=env, capture_output=True, text=True)
+            line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:]
+            print(f"{v:14s} {line}", flush=True)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
