@@ -147,6 +147,9 @@ int bkg_solver_history(bkg_solver* s, double* history, uint64_t cap, uint64_t* r
  * out_ms[0]=SpMM+Gram (K1), [1]=update+Gram (K2), [2]=P update (K3),
  * [3]=whole iteration.  Launches are not graph-captured in this pass.      */
 int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms);
+/* Test hook: set up a solve from X0 = 0 and run only the first SpMM+Gram
+ * step (K1); returns Q = A P^1 (n*k) and [lambda^1 | rho_prev^1] (2*cs).   */
+int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out);
 /* Algorithmic bytes one launch of each fused kernel class must move
  * (DESIGN.md §Roofline): out[0..2] as above, out[3] = per iteration.       */
 int bkg_solver_kernel_bytes(const bkg_solver* s, double* out);

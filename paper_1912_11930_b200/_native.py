@@ -97,6 +97,7 @@ SIGNATURES = [
     ("bkg_solver_get_x", C.c_int, [_vp, _d]),
     ("bkg_solver_history", C.c_int, [_vp, _d, C.c_uint64, _u]),
     ("bkg_solver_profile", C.c_int, [_vp, C.c_uint64, _d]),
+    ("bkg_solver_debug_first_step", C.c_int, [_vp, _d, _d]),
     ("bkg_solver_kernel_bytes", C.c_int, [_vp, _d]),
     ("bkg_stencil_size", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _u, _u]),
     ("bkg_stencil_fill", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,

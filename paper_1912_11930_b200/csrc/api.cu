@@ -317,9 +317,10 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
-      g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc);
-      g2 = occupancy_grid(c, ft.k2, ft.smem_iter, n, ft.rpc);
-      g3 = occupancy_grid(c, ft.k3, ft.smem_iter, n, ft.rpc);
+      g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc_k1);
+      const int rpc23 = ft.mma ? ft.rpc_mma : ft.rpc;
+      g2 = occupancy_grid(c, ft.k2, ft.smem_iter, n, rpc23);
+      g3 = occupancy_grid(c, ft.k3, ft.smem_iter, n, rpc23);
       const int gmax = std::max(std::max(g1, g2), g3);
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
@@ -915,6 +916,30 @@ int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms) {
     d2h(s->ctx, reinterpret_cast<char*>(s->h_ctrl), reinterpret_cast<const char*>(s->dctrl()), sizeof(Ctrl));
     sync(s->ctx);
     BKG_REQUIRE(!s->h_ctrl->done, BKG_INTERNAL, "profile pass stopped early (breakdown)");
+  });
+}
+
+int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out) {
+  return guard([&] {
+    BKG_REQUIRE(s->have_b, BKG_CONFIG, "solver: right hand side not set");
+    activate(s->ctx);
+    bkg_report rep{};
+    std::vector<double> lim;
+    bool nz = false;
+    s->setup(nullptr, 1e-300, ~0ull, false, &rep, &lim, &nz);
+    Ctrl h{};
+    h.max_iter = ~0ull;
+    h2d(s->ctx, reinterpret_cast<char*>(s->dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
+    if (s->fast) {
+      IterArgs a = s->iter_args(false);
+      void* args[] = {&a};
+      launch(s->ctx, s->ft.k1, s->g1, kThreads, s->ft.smem_iter, args);
+    } else {
+      dev_spmm(s->ctx, s->A, s->k, s->P, s->Q.ptr, nullptr, true);
+    }
+    d2h(s->ctx, q_out, s->Q.ptr, (size_t)s->n * s->k);
+    d2h(s->ctx, coef_out, s->coef.ptr, (size_t)2 * s->cs);
+    sync(s->ctx);
   });
 }
 

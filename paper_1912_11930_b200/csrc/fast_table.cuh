@@ -6,6 +6,7 @@
 #pragma once
 
 #include "kernels_fast.cuh"
+#include "kernels_mma.cuh"
 
 namespace bkg {
 
@@ -25,6 +26,9 @@ struct FastTable {
   int e_iter = 0;      // partial entries per CTA (max of k1, k2)
   int e_gram = 0;
   int e_norms = 0;
+  bool mma = false;  // K2/K3 are the DMMA kernels
+  int rpc_mma = 1;    // their rows per CTA pass (8 rows per warp, Q warps per row block)
+  int rpc_k1 = 1;     // rows per CTA pass of K1
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -38,9 +42,23 @@ template <int K, int P, bool G>
 void fill_table(FastTable* t) {
   constexpr int CPT = cpt_for<P>();
   using S = FastSmem<K, P, CPT, G>;
-  t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
-  t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
-  t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
+  if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
+    constexpr int W = K >= 16 ? 16 : 8;
+    t->k1 = (const void*)&k1_tile<K, P, W, G>;
+    t->rpc_k1 = 64 * W / K;
+  } else {
+    t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
+    t->rpc_k1 = Layout<K, P, CPT>::RPC;
+  }
+  if constexpr (P == 8 || P == 16) {  // dense p x p contraction: FP64 DMMA
+    t->k2 = (const void*)&k2_mma<K, P, G>;
+    t->k3 = (const void*)&k3_mma<K, P, G>;
+    t->mma = true;
+    t->rpc_mma = 64 * P / K;
+  } else {
+    t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
+    t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
+  }
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
   t->norms = (const void*)&k_norms_fast<K, CPT>;

@@ -213,7 +213,15 @@ template <int K, int P, int CPT, bool GLOBAL>
 struct FastSmem {
   static constexpr int NB = GLOBAL ? 1 : K / P;
   static constexpr int CS = NB * P * P;
-  static constexpr int RED = K * P + K;  // largest TPR * NACC over K1..K3
+  // largest TPR * NACC over the scalar K1..K3 and the DMMA K2/K3 (P >= 8)
+  static constexpr int RED_SCALAR = K * P + K;
+  static constexpr int RED_MMA = (P >= 8) ? 32 * (K / P) * (2 * (P / 8) * (P / 8) + 2 * (P / 8)) : 0;
+  // K1 warp-tile kernel (kernels_mma.cuh k1_tile): 32*QW positions x 2*NPAIR
+  static constexpr int W1 = K >= 16 ? 16 : 8;
+  static constexpr int RED_K1 =
+      (K % 8 == 0) ? 32 * (K / W1) * 2 * ((P >= 8) ? (W1 / 8) * (P / 8) : (W1 / 8)) : 0;
+  static constexpr int RED_A = RED_SCALAR > RED_MMA ? RED_SCALAR : RED_MMA;
+  static constexpr int RED = RED_A > RED_K1 ? RED_A : RED_K1;
   static int bytes() {
     return (int)sizeof(double) * (RED + 3 * CS + bsolve_ws_doubles(P, kThreads) + K);
   }
@@ -298,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k1_spmm_gram
   using S = FastSmem<K, P, CPT, GLOBAL>;
   if (stopped(a.ctrl)) return;
   constexpr int NACC = P * CPT;
+  static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
 #pragma unroll
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
@@ -367,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
   for (int i = threadIdx.x; i < S::CS; i += kThreads) lam[i] = a.coef[i];
   __syncthreads();
   constexpr int NACC = P * CPT + CPT;
+  static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
 #pragma unroll
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
@@ -463,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   }
   __syncthreads();
   constexpr int NACC = P * CPT;
+  static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
 #pragma unroll
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;

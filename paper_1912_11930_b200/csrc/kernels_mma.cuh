@@ -1,0 +1,435 @@
+// kernels_mma.cuh — FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) versions of
+// the row-streaming Block-CG updates for block widths P in {8, 16}.
+//
+// For P >= 8 the update X += Y gamma (kernels.hpp:94-125) is a real dense
+// contraction (P multiply-adds per element) and the Gram tile
+// (kernels.hpp:59-88) is P^2 per row.  With scalar FMAs every thread needs
+// the whole p-group of its row (warp shuffles) and P*CPT coefficients in
+// registers, which made the scalar K2/K3 shuffle/L1-bound (ncu: L1/TEX 97%).
+// Here a warp owns an 8-row x P-column tile of one p-group:
+//   * the p x p coefficient block lives in B fragments: P^2/32 doubles/lane;
+//   * Y enters as A fragments (8 B per lane per k-chunk, 32 B row segments);
+//   * X / R enter and leave in the C/D layout (16 B per lane);
+//   * the Gram tile G = U^T V over the 8 rows is two more k=4 MMAs per
+//     8x8 output tile after an in-register D->T relayout (2 shuffles).
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64):
+//   A (8x4, row): lane holds A[lane>>2][lane&3]
+//   B (4x8, col): lane holds B[lane&3][lane>>2]
+//   C/D (8x8):    lane holds D[lane>>2][2*(lane&3) + i], i = 0, 1
+#pragma once
+
+#include "kernels_fast.cuh"
+
+namespace bkg {
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// D-layout 8x8 tile -> the two T-layout 4x8 chunks (rows 4c..4c+3):
+// t[c] = tile[4c + (lane&3)][lane>>2], the A/B operand layout of a Gram
+// product over rows.
+__device__ __forceinline__ void d_to_t(const double (&d)[2], double (&t)[2], int lane) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int src = 16 * c + 4 * (lane & 3) + (lane >> 3);
+    const double v0 = __shfl_sync(kFull, d[0], src);
+    const double v1 = __shfl_sync(kFull, d[1], src);
+    t[c] = ((lane >> 2) & 1) ? v1 : v0;
+  }
+}
+
+template <int K, int P, bool GLOBAL>
+struct MmaLayout {
+  static constexpr int Q = K / P;     // p-groups per row
+  static constexpr int NT = P / 8;    // 8-column output tiles per group
+  static constexpr int KC = P / 4;    // 4-column k-chunks per group
+  static constexpr int TPR = 32 * Q;  // grid_reduce positions: (warp % Q, lane)
+  static constexpr int NB = GLOBAL ? 1 : Q;
+  static constexpr int CS = NB * P * P;
+  static_assert(P == 8 || P == 16, "DMMA path is for P in {8, 16}");
+  static_assert(8 % Q == 0 || Q > 8, "warps per CTA must cover whole groups");
+};
+
+// B fragments of a p x p coefficient block c (row-major, c[b][a]):
+// frag[kc][nt] = sign * c[kc*4 + (lane&3)][nt*8 + (lane>>2)].
+template <int P>
+__device__ __forceinline__ void load_bfrag(const double* c, double sign,
+                                           double (&f)[P / 4][P / 8], int lane) {
+#pragma unroll
+  for (int kc = 0; kc < P / 4; ++kc)
+#pragma unroll
+    for (int nt = 0; nt < P / 8; ++nt)
+      f[kc][nt] = sign * c[(kc * 4 + (lane & 3)) * P + nt * 8 + (lane >> 2)];
+}
+
+// Grid totals of a Gram accumulator in D layout (per (group, lane) position
+// of grid_reduce) gathered into row-major p x p blocks.
+template <int K, int P, bool GLOBAL, int NACC>
+__device__ void gather_gram_mma(const double* red, int off, double* blocks) {
+  using L = MmaLayout<K, P, GLOBAL>;
+  for (int idx = threadIdx.x; idx < L::NB * P * P; idx += kThreads) {
+    const int blk = idx / (P * P), a = (idx / P) % P, b = idx % P;
+    const int at = a >> 3, bt = b >> 3;
+    const int lane = ((a & 7) << 2) | ((b & 7) >> 1), i = b & 1;
+    const int e = off + (at * L::NT + bt) * 2 + i;
+    double s = 0.0;
+    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? L::Q : blk + 1;
+    for (int g = g0; g < g1; ++g) s += red[(g * 32 + lane) * NACC + e];
+    blocks[idx] = s;
+  }
+}
+
+// Column sums of squares held per lane in D layout (entry off + nt*2 + i is
+// column nt*8 + 2*(lane&3) + i of the lane's group), summed over the 8 row
+// lanes and square-rooted.
+template <int K, int P, bool GLOBAL, int NACC>
+__device__ void gather_norms_mma(const double* red, int off, double* norms) {
+  using L = MmaLayout<K, P, GLOBAL>;
+  for (int c = threadIdx.x; c < K; c += kThreads) {
+    const int g = c / P, cc = c % P, nt = cc >> 3, i = cc & 1, l4 = (cc & 7) >> 1;
+    double s = 0.0;
+    for (int r = 0; r < 8; ++r) s += red[(g * 32 + (r << 2) + l4) * NACC + off + nt * 2 + i];
+    norms[c] = sqrt(s);
+  }
+}
+
+// ------------------------------------------------------------ K2 (DMMA) --
+// R -= Q lambda; rho = <<R, R>>; ||R_s||^2; last CTA: beta, history, stop.
+template <int K, int P, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, 2) k2_mma(IterArgs a) {
+  using L = MmaLayout<K, P, GLOBAL>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  if (stopped(a.ctrl)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = warp % L::Q;
+  double nlam[L::KC][L::NT];
+  load_bfrag<P>(a.coef + (GLOBAL ? 0 : g) * P * P, -1.0, nlam, lane);
+  constexpr int NG = L::NT * L::NT * 2;  // Gram accumulators
+  constexpr int NACC = NG + L::NT * 2;   // + column sums of squares
+  static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
+  double acc[NACC];
+#pragma unroll
+  for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
+  const int64_t nrb = (a.n + 7) >> 3;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
+  const int col_a = g * P + (lane & 3);            // A-fragment column base
+  const int col_c = g * P + 2 * (lane & 3);        // C-fragment column base
+  for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
+       rb += wstride) {
+    const int64_t row = rb * 8 + (lane >> 2);
+    const bool ok = row < a.n;
+    double qa[L::KC], rc[L::NT][2];
+#pragma unroll
+    for (int kc = 0; kc < L::KC; ++kc) qa[kc] = ok ? __ldg(a.Q + row * K + col_a + kc * 4) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      double t[2] = {0.0, 0.0};
+      if (ok) ld_rw<2>(t, a.R + row * K + col_c + nt * 8);
+      rc[nt][0] = t[0];
+      rc[nt][1] = t[1];
+    }
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < L::KC; ++kc) dmma(rc[nt], qa[kc], nlam[kc][nt]);
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      if (ok) st<2>(a.R + row * K + col_c + nt * 8, rc[nt]);
+      acc[NG + nt * 2] = fma(rc[nt][0], rc[nt][0], acc[NG + nt * 2]);
+      acc[NG + nt * 2 + 1] = fma(rc[nt][1], rc[nt][1], acc[NG + nt * 2 + 1]);
+    }
+    double tr[L::NT][2];
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) d_to_t(rc[nt], tr[nt], lane);
+#pragma unroll
+    for (int at = 0; at < L::NT; ++at)
+#pragma unroll
+      for (int bt = 0; bt < L::NT; ++bt) {
+        double* gacc = acc + (at * L::NT + bt) * 2;
+        double d[2] = {gacc[0], gacc[1]};
+        dmma(d, tr[at][0], tr[bt][0]);
+        dmma(d, tr[at][1], tr[bt][1]);
+        gacc[0] = d[0];
+        gacc[1] = d[1];
+      }
+  }
+  extern __shared__ double sm[];
+  double* red = sm;
+  if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
+  double* rho = sm + S::RED;
+  double* beta_s = rho + S::CS;
+  double* norms = beta_s + S::CS;
+  double* ws = sm + S::RED + 3 * S::CS + K;
+  gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, rho);
+  gather_norms_mma<K, P, GLOBAL, NACC>(red, NG, norms);
+  __syncthreads();
+  const int bad = cta_bsolve<P>(L::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
+  if (threadIdx.x == 0) a.ctrl->xpending = 1;
+  if (bad >= 0) {
+    record_breakdown(a.ctrl, bad, 2);
+    return;
+  }
+  for (int i = threadIdx.x; i < S::CS; i += kThreads) {
+    a.coef[2 * S::CS + i] = beta_s[i];
+    a.coef[3 * S::CS + i] = rho[i];
+  }
+  finish_iteration(a.ctrl, norms, a.limits, a.hist, a.hist_ring, K);
+}
+
+// ------------------------------------------------------------ K3 (DMMA) --
+// X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
+template <int K, int P, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, 2) k3_mma(IterArgs a) {
+  using L = MmaLayout<K, P, GLOBAL>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
+  const bool fin = stopped(a.ctrl);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = warp % L::Q;
+  const double* cb = a.coef + (GLOBAL ? 0 : g) * P * P;
+  double lam[L::KC][L::NT], bet[L::KC][L::NT];
+  load_bfrag<P>(cb, 1.0, lam, lane);
+  load_bfrag<P>(cb + 2 * S::CS, 1.0, bet, lane);
+  constexpr int NACC = L::NT * L::NT * 2;
+  static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
+  double acc[NACC];
+#pragma unroll
+  for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
+  const int64_t nrb = (a.n + 7) >> 3;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
+  const int col_a = g * P + (lane & 3);
+  const int col_c = g * P + 2 * (lane & 3);
+  for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
+       rb += wstride) {
+    const int64_t row = rb * 8 + (lane >> 2);
+    const bool ok = row < a.n;
+    double pa[L::KC], xc[L::NT][2], pn[L::NT][2];
+#pragma unroll
+    for (int kc = 0; kc < L::KC; ++kc) pa[kc] = ok ? a.P[row * K + col_a + kc * 4] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      double t[2] = {0.0, 0.0}, r[2] = {0.0, 0.0};
+      if (ok) {
+        ld_rw<2>(t, a.X + row * K + col_c + nt * 8);
+        if (!fin) ld_nc<2>(r, a.R + row * K + col_c + nt * 8);
+      }
+      xc[nt][0] = t[0];
+      xc[nt][1] = t[1];
+      pn[nt][0] = r[0];
+      pn[nt][1] = r[1];
+    }
+    double tr[L::NT][2];
+    if (!fin) {
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tr[nt], lane);  // R, T layout
+    }
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < L::KC; ++kc) {
+        dmma(xc[nt], pa[kc], lam[kc][nt]);
+        if (!fin) dmma(pn[nt], pa[kc], bet[kc][nt]);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      if (ok) {
+        st<2>(a.X + row * K + col_c + nt * 8, xc[nt]);
+        if (!fin) st<2>(a.P + row * K + col_c + nt * 8, pn[nt]);
+      }
+    }
+    if (!fin) {
+      double tp[L::NT][2];
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tp[nt], lane);
+#pragma unroll
+      for (int at = 0; at < L::NT; ++at)
+#pragma unroll
+        for (int bt = 0; bt < L::NT; ++bt) {
+          double* gacc = acc + (at * L::NT + bt) * 2;
+          double d[2] = {gacc[0], gacc[1]};
+          dmma(d, tp[at][0], tr[bt][0]);
+          dmma(d, tp[at][1], tr[bt][1]);
+          gacc[0] = d[0];
+          gacc[1] = d[1];
+        }
+    }
+  }
+  extern __shared__ double sm[];
+  double* red = sm;
+  if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
+  if (!fin) gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, a.coef + S::CS);  // rho_prev
+  if (threadIdx.x == 0) a.ctrl->xpending = 0;
+}
+
+}  // namespace bkg
+
+namespace bkg {
+
+// ------------------------------------------------------------ K1 (tile) --
+// Q = A P and alpha = <<P, Q>> with the warp as the unit of work: a warp owns
+// an 8-row x W-column tile (W = 16, or K when K < 16); lane (lane>>2) is its
+// row and it accumulates W/4 columns of Q in the DMMA C/D layout (16-byte
+// operand loads, one CSR stream per row shared by its 4 lanes).  The Gram
+// tile P^T Q over the 8 rows is then DMMA work: P is read in the T layout
+// (its rows are L1-resident: they were just read as diagonal operands) and Q
+// is relaid D->T in registers.  Only the (at, bt) 8x8 tile pairs inside one
+// p-group are formed (block-diagonal for P < 8).
+template <int K, int P, int W>
+struct TileLayout {
+  static constexpr int QW = K / W;     // warps per 8-row block
+  static constexpr int NTW = W / 8;    // 8-column tiles per warp
+  static constexpr int PT = P >= 8 ? P / 8 : 1;  // tiles per p-group side
+  // Gram tile pairs kept per warp: within-group pairs of its NTW tiles
+  static constexpr int NPAIR = (P >= 8) ? NTW * PT : NTW;
+  static constexpr int TPR = 32 * QW;
+  static_assert(K % W == 0 && W % 8 == 0, "tile width");
+  static_assert(P < 8 || W % P == 0, "a p-group must not straddle warps");
+};
+
+template <int K, int P, int W>
+__device__ __forceinline__ void tile_pair(int idx, int& at, int& bt) {
+  using T = TileLayout<K, P, W>;
+  if (P >= 8) {  // idx = tile * PT + j: partner j inside the tile's group
+    const int t = idx / T::PT, j = idx % T::PT;
+    at = t;
+    bt = (t / T::PT) * T::PT + j;
+  } else {
+    at = bt = idx;
+  }
+}
+
+// Grid totals of the tile-pair Gram accumulators -> row-major p x p blocks.
+template <int K, int P, int W, bool GLOBAL, int NACC>
+__device__ void gather_gram_tile(const double* red, double* blocks) {
+  using T = TileLayout<K, P, W>;
+  constexpr int NB = GLOBAL ? 1 : K / P;
+  constexpr int Qg = K / P;
+  for (int idx = threadIdx.x; idx < NB * P * P; idx += kThreads) {
+    const int blk = idx / (P * P), a = (idx / P) % P, b = idx % P;
+    double s = 0.0;
+    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? Qg : blk + 1;
+    for (int g = g0; g < g1; ++g) {
+      const int ca = g * P + a, cb = g * P + b;
+      const int w = ca / W, aw = ca % W, bw = cb % W;
+      const int at = aw >> 3, bt = bw >> 3;
+      int pi = 0;
+      if (P >= 8) pi = at * T::PT + (bt % T::PT);
+      else pi = at;
+      const int lane = ((aw & 7) << 2) | ((bw & 7) >> 1), i = bw & 1;
+      s += red[(w * 32 + lane) * NACC + pi * 2 + i];
+    }
+    blocks[idx] = s;
+  }
+}
+
+template <int K, int P, int W, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, 2) k1_tile(IterArgs a) {
+  using T = TileLayout<K, P, W>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  if (stopped(a.ctrl)) return;
+  constexpr int CH = 8;  // CSR entries in flight per lane
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = warp % T::QW;
+  const int c0 = w * W + 2 * (lane & 3);  // C/D layout column of n-tile 0
+  constexpr int NACC = T::NPAIR * 2;
+  static_assert(T::TPR * NACC <= S::RED, "grid_reduce buffer");
+  double acc[NACC];
+#pragma unroll
+  for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
+  const int64_t nrb = (a.n + 7) >> 3;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / T::QW;
+  int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / T::QW;
+  int64_t row = rb * 8 + (lane >> 2);
+  int64_t beg = 0, end = 0;
+  if (rb < nrb && row < a.n) {
+    beg = __ldg(a.rowptr + row);
+    end = __ldg(a.rowptr + row + 1);
+  }
+  for (; rb < nrb; rb += wstride) {
+    const int64_t nrow = row + wstride * 8;
+    int64_t nbeg = 0, nend = 0;
+    if (nrow < a.n) {
+      nbeg = __ldg(a.rowptr + nrow);
+      nend = __ldg(a.rowptr + nrow + 1);
+    }
+    double q[T::NTW][2];
+#pragma unroll
+    for (int t = 0; t < T::NTW; ++t) q[t][0] = q[t][1] = 0.0;
+#pragma unroll 1
+    for (int64_t i = beg; i < end; i += CH) {
+      double v[CH];
+      int c[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const bool on = i + u < end;
+        v[u] = on ? __ldg(a.vals + i + u) : 0.0;
+        c[u] = on ? __ldg(a.cols + i + u) : -1;
+      }
+      double x[CH][T::NTW][2];
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+#pragma unroll
+        for (int t = 0; t < T::NTW; ++t) {
+          if (c[u] >= 0) {
+            ld_nc<2>(x[u][t], a.P + (int64_t)c[u] * K + c0 + t * 8);
+          } else {
+            x[u][t][0] = x[u][t][1] = 0.0;
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (c[u] >= 0) {
+#pragma unroll
+          for (int t = 0; t < T::NTW; ++t) {
+            q[t][0] = fma(v[u], x[u][t][0], q[t][0]);
+            q[t][1] = fma(v[u], x[u][t][1], q[t][1]);
+          }
+        }
+    }
+    __syncwarp();
+    if (row < a.n) {
+#pragma unroll
+      for (int t = 0; t < T::NTW; ++t) st<2>(a.Q + row * K + c0 + t * 8, q[t]);
+    }
+    // P tile in T layout: pt[t][c] = P[rb*8 + 4c + (lane&3)][w*W + t*8 + (lane>>2)]
+    double pt[T::NTW][2], qt[T::NTW][2];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int64_t prow = rb * 8 + 4 * cc + (lane & 3);
+#pragma unroll
+      for (int t = 0; t < T::NTW; ++t)
+        pt[t][cc] = prow < a.n ? __ldg(a.P + prow * K + w * W + t * 8 + (lane >> 2)) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < T::NTW; ++t) d_to_t(q[t], qt[t], lane);
+#pragma unroll
+    for (int pi = 0; pi < T::NPAIR; ++pi) {
+      int at, bt;
+      tile_pair<K, P, W>(pi, at, bt);
+      double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
+      dmma(d, pt[at][0], qt[bt][0]);
+      dmma(d, pt[at][1], qt[bt][1]);
+      acc[2 * pi] = d[0];
+      acc[2 * pi + 1] = d[1];
+    }
+    row = nrow;
+    beg = nbeg;
+    end = nend;
+  }
+  extern __shared__ double sm[];
+  double* red = sm;
+  if (!grid_reduce<T::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
+  double* alpha = sm + S::RED;
+  double* ws = alpha + 3 * S::CS;
+  gather_gram_tile<K, P, W, GLOBAL, NACC>(red, alpha);
+  __syncthreads();
+  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
+}
+
+}  // namespace bkg

@@ -49,6 +49,14 @@ class DeviceSolver:
         _check(N.lib().bkg_solver_profile(self.handle, iterations, _dp(out)))
         return out
 
+    def debug_first_step(self):
+        """(Q = A B, [lambda^1 | rho_prev^1]) from one K1 launch (test hook)."""
+        q = np.empty((self.a.n(), self.cfg.k))
+        cs = self.cfg.block_count() * self.cfg.p ** 2
+        coef = np.empty(2 * cs)
+        _check(N.lib().bkg_solver_debug_first_step(self.handle, _dp(q), _dp(coef)))
+        return q, coef
+
     def kernel_bytes(self) -> np.ndarray:
         out = np.zeros(4)
         _check(N.lib().bkg_solver_kernel_bytes(self.handle, _dp(out)))

@@ -234,7 +234,11 @@ def test_hybrid_splits_into_independent_classical_runs(ctx):
         cl = _iterates(a, b[:, 4 * g:4 * g + 4].copy(), bk.SubalgebraConfig.classical(4), 20, ctx)
         assert len(cl) == len(hy)
         for i in range(len(hy)):
-            assert np.max(np.abs(hy[i][:, 4 * g:4 * g + 4] - cl[i])) <= 1e-12
+            # exact mode keeps the reference's per-entry order: identical runs
+            # (test_solver.cpp:228, 1e-12); fast mode reduces the k=8 and k=4
+            # Gram tiles with different trees, so allow rounding-level drift.
+            tol = 1e-12 if ctx.numerics == "exact" else 1e-10
+            assert np.max(np.abs(hy[i][:, 4 * g:4 * g + 4] - cl[i])) <= tol
 
 
 def test_global_equals_classical_on_stacked_system(ctx):
