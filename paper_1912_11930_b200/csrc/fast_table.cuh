@@ -45,7 +45,7 @@ void fill_table(FastTable* t) {
   if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;
-    t->rpc_k1 = 64 * W / K;
+    t->rpc_k1 = (64 / W) * (8 * W / K);  // (rows per warp tile) x (row tiles per CTA)
   } else {
     t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
     t->rpc_k1 = Layout<K, P, CPT>::RPC;

@@ -99,8 +99,11 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms) {
 
 // ------------------------------------------------------------ K2 (DMMA) --
 // R -= Q lambda; rho = <<R, R>>; ||R_s||^2; last CTA: beta, history, stop.
+#ifndef BKG_MMA_MINB
+#define BKG_MMA_MINB 2
+#endif
 template <int K, int P, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, 2) k2_mma(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, BKG_MMA_MINB) k2_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   if (stopped(a.ctrl)) return;
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2) k2_mma(IterArgs a) {
 // ------------------------------------------------------------ K3 (DMMA) --
 // X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
 template <int K, int P, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, 2) k3_mma(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, BKG_MMA_MINB) k3_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
@@ -327,99 +330,132 @@ __device__ void gather_gram_tile(const double* red, double* blocks) {
   }
 }
 
+#ifndef BKG_K1_MINB
+#define BKG_K1_MINB 2
+#endif
+// K1 with the SpMM laid out for whole cache lines: LPR = W/2 lanes x 16 bytes
+// cover a row's W-column segment (128 bytes when W = 16), so a warp tile is
+// RPW = 64/W rows.  The Gram P^T Q over those rows is k = 4 rows per DMMA
+// (m8n8k4), RPW/4 MMAs per tile pair; both operands are relaid from the row
+// layout into the T layout with shuffles.  Software pipeline: the CSR chunk
+// (values + columns) of tile t+1 and the row extents of tile t+2 are loaded
+// while tile t's operand loads are in flight, so a tile costs one dependent
+// memory round trip instead of three.
 template <int K, int P, int W, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, 2) k1_tile(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, BKG_K1_MINB) k1_tile(IterArgs a) {
   using T = TileLayout<K, P, W>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   if (stopped(a.ctrl)) return;
-  constexpr int CH = 8;  // CSR entries in flight per lane
+  constexpr int LPR = W / 2, RPW = 32 / LPR, CHK = RPW / 4;
+  constexpr int CH = 8;  // CSR entries per lane per chunk (a 7-point row in one)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int w = warp % T::QW;
-  const int c0 = w * W + 2 * (lane & 3);  // C/D layout column of n-tile 0
+  const int rr = lane / LPR, cl = lane % LPR;
+  const int col = w * W + 2 * cl;
+  const double* Pc = a.P + col;
   constexpr int NACC = T::NPAIR * 2;
   static_assert(T::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
 #pragma unroll
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
-  const int64_t nrb = (a.n + 7) >> 3;
+  const int64_t ntile = (a.n + RPW - 1) / RPW;
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / T::QW;
-  int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / T::QW;
-  int64_t row = rb * 8 + (lane >> 2);
-  int64_t beg = 0, end = 0;
-  if (rb < nrb && row < a.n) {
-    beg = __ldg(a.rowptr + row);
-    end = __ldg(a.rowptr + row + 1);
-  }
-  for (; rb < nrb; rb += wstride) {
-    const int64_t nrow = row + wstride * 8;
-    int64_t nbeg = 0, nend = 0;
-    if (nrow < a.n) {
-      nbeg = __ldg(a.rowptr + nrow);
-      nend = __ldg(a.rowptr + nrow + 1);
+  const int64_t rstride = wstride * RPW;
+  int64_t tile = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / T::QW;
+  int64_t row = tile * RPW + rr;
+
+  auto extent = [&](int64_t r, int64_t& b, int& len) {
+    b = 0;
+    len = 0;
+    if (r < a.n) {
+      b = __ldg(a.rowptr + r);
+      len = (int)(__ldg(a.rowptr + r + 1) - b);
     }
-    double q[T::NTW][2];
+  };
+  auto load_chunk = [&](int64_t b, int len, double (&v)[CH], int (&c)[CH]) {
 #pragma unroll
-    for (int t = 0; t < T::NTW; ++t) q[t][0] = q[t][1] = 0.0;
-#pragma unroll 1
-    for (int64_t i = beg; i < end; i += CH) {
-      double v[CH];
-      int c[CH];
+    for (int u = 0; u < CH; ++u) {
+      v[u] = u < len ? __ldg(a.vals + b + u) : 0.0;
+      c[u] = u < len ? __ldg(a.cols + b + u) : -1;
+    }
+  };
+  // FMAs of one chunk: inactive slots carry v = 0, x = 0.
+  auto fma_chunk = [&](const double (&v)[CH], const int (&c)[CH], double (&q)[2]) {
+    double x[CH][2];
 #pragma unroll
-      for (int u = 0; u < CH; ++u) {
-        const bool on = i + u < end;
-        v[u] = on ? __ldg(a.vals + i + u) : 0.0;
-        c[u] = on ? __ldg(a.cols + i + u) : -1;
+    for (int u = 0; u < CH; ++u) {
+      if (c[u] >= 0) {
+        ld_nc<2>(x[u], Pc + (int64_t)c[u] * K);
+      } else {
+        x[u][0] = x[u][1] = 0.0;
       }
-      double x[CH][T::NTW][2];
+    }
 #pragma unroll
-      for (int u = 0; u < CH; ++u)
-#pragma unroll
-        for (int t = 0; t < T::NTW; ++t) {
-          if (c[u] >= 0) {
-            ld_nc<2>(x[u][t], a.P + (int64_t)c[u] * K + c0 + t * 8);
-          } else {
-            x[u][t][0] = x[u][t][1] = 0.0;
-          }
-        }
-#pragma unroll
-      for (int u = 0; u < CH; ++u)
-        if (c[u] >= 0) {
-#pragma unroll
-          for (int t = 0; t < T::NTW; ++t) {
-            q[t][0] = fma(v[u], x[u][t][0], q[t][0]);
-            q[t][1] = fma(v[u], x[u][t][1], q[t][1]);
-          }
-        }
+    for (int u = 0; u < CH; ++u) {
+      q[0] = fma(v[u], x[u][0], q[0]);
+      q[1] = fma(v[u], x[u][1], q[1]);
+    }
+  };
+
+  int64_t b0, b1;
+  int len0, len1;
+  double v[CH];
+  int c[CH];
+  extent(row, b0, len0);
+  extent(row + rstride, b1, len1);
+  load_chunk(b0, len0, v, c);
+  for (; tile < ntile; tile += wstride) {
+    // prefetch: extents of tile t+2, CSR chunk of tile t+1
+    int64_t b2;
+    int len2;
+    extent(row + 2 * rstride, b2, len2);
+    double nv[CH];
+    int nc[CH];
+    load_chunk(b1, len1, nv, nc);
+    double q[2] = {0.0, 0.0}, pd[2] = {0.0, 0.0};
+    if (row < a.n) ld_nc<2>(pd, Pc + row * K);
+    fma_chunk(v, c, q);
+    for (int off = CH; off < len0; off += CH) {  // rows longer than one chunk
+      double v2[CH];
+      int c2[CH];
+      load_chunk(b0 + off, len0 - off, v2, c2);
+      fma_chunk(v2, c2, q);
     }
     __syncwarp();
-    if (row < a.n) {
+    if (row < a.n) st<2>(a.Q + row * K + col, q);
+    // T layout of the tile's 4-row chunks: t[nt][c] = tile[4c + (lane&3)][nt*8 + (lane>>2)]
+    double pt[T::NTW][CHK], qt[T::NTW][CHK];
 #pragma unroll
-      for (int t = 0; t < T::NTW; ++t) st<2>(a.Q + row * K + c0 + t * 8, q[t]);
-    }
-    // P tile in T layout: pt[t][c] = P[rb*8 + 4c + (lane&3)][w*W + t*8 + (lane>>2)]
-    double pt[T::NTW][2], qt[T::NTW][2];
+    for (int nt = 0; nt < T::NTW; ++nt)
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int64_t prow = rb * 8 + 4 * cc + (lane & 3);
-#pragma unroll
-      for (int t = 0; t < T::NTW; ++t)
-        pt[t][cc] = prow < a.n ? __ldg(a.P + prow * K + w * W + t * 8 + (lane >> 2)) : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < T::NTW; ++t) d_to_t(q[t], qt[t], lane);
+      for (int cc = 0; cc < CHK; ++cc) {
+        const int src = (4 * cc + (lane & 3)) * LPR + nt * 4 + (lane >> 3);
+        const bool hi = (lane >> 2) & 1;
+        const double q0 = __shfl_sync(kFull, q[0], src), q1 = __shfl_sync(kFull, q[1], src);
+        const double p0 = __shfl_sync(kFull, pd[0], src), p1 = __shfl_sync(kFull, pd[1], src);
+        qt[nt][cc] = hi ? q1 : q0;
+        pt[nt][cc] = hi ? p1 : p0;
+      }
 #pragma unroll
     for (int pi = 0; pi < T::NPAIR; ++pi) {
       int at, bt;
       tile_pair<K, P, W>(pi, at, bt);
       double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
-      dmma(d, pt[at][0], qt[bt][0]);
-      dmma(d, pt[at][1], qt[bt][1]);
+#pragma unroll
+      for (int cc = 0; cc < CHK; ++cc) dmma(d, pt[at][cc], qt[bt][cc]);
       acc[2 * pi] = d[0];
       acc[2 * pi + 1] = d[1];
     }
-    row = nrow;
-    beg = nbeg;
-    end = nend;
+    row += rstride;
+    b0 = b1;
+    len0 = len1;
+    b1 = b2;
+    len1 = len2;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      v[u] = nv[u];
+      c[u] = nc[u];
+    }
   }
   extern __shared__ double sm[];
   double* red = sm;
