@@ -99,11 +99,15 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms) {
 
 // ------------------------------------------------------------ K2 (DMMA) --
 // R -= Q lambda; rho = <<R, R>>; ||R_s||^2; last CTA: beta, history, stop.
-#ifndef BKG_MMA_MINB
-#define BKG_MMA_MINB 2
-#endif
+// Resident CTAs per SM (register cap) for the DMMA K2/K3, measured on B200
+// (tools/kernel_sweep.py): P = 8 tiles are small enough for 4 CTAs (64 regs);
+// at P = 16, K2 peaks at 3 and K3 (two coefficient blocks) at 2.
+template <int P, int KERNEL>
+constexpr int mma_minb() {
+  return P == 8 ? 4 : (KERNEL == 2 ? 3 : 2);
+}
 template <int K, int P, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, BKG_MMA_MINB) k2_mma(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   if (stopped(a.ctrl)) return;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, BKG_MMA_MINB) k2_mma(IterArgs a) {
 // ------------------------------------------------------------ K3 (DMMA) --
 // X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
 template <int K, int P, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, BKG_MMA_MINB) k3_mma(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
