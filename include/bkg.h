@@ -154,6 +154,39 @@ int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out);
  * (DESIGN.md §Roofline): out[0..2] as above, out[3] = per iteration.       */
 int bkg_solver_kernel_bytes(const bkg_solver* s, double* out);
 
+/* ---- row-partitioned solver (multi-GPU) --------------------- */
+/* Rows are split into contiguous blocks ("parts"); each part keeps its rows
+ * of X, R, Q and a ghost-extended P.  Per iteration: halo exchange of P,
+ * SpMM + local Gram partials, allreduce of [alpha|rho_prev] and
+ * [rho|col norms^2], replicated p x p solves.  Fast numerics only.         */
+typedef struct bkg_psolver bkg_psolver;
+/* Halo plan for nparts contiguous row blocks row_begin[0..nparts]: part r
+ * needs operand rows [need_lo[r], need_hi[r]).  Writes `count` copies
+ * (dst, src, first row, rows) into out (4 int64 each, up to cap).          */
+int bkg_halo_plan(int nparts, const int64_t* row_begin, const int64_t* need_lo,
+                  const int64_t* need_hi, int64_t* out, uint64_t cap, uint64_t* count);
+/* NCCL unique id (128 bytes) for bkg_psolver_create_nccl, made on rank 0.  */
+int bkg_nccl_unique_id(void* id_out);
+/* All parts on this context's device (single-GPU emulation of nparts ranks;
+ * halo = device copies, allreduce = fixed-order sum).  Global CSR in.      */
+int bkg_psolver_create_virtual(bkg_ctx* ctx, uint64_t n, const uint64_t* row_offsets,
+                               const uint64_t* cols, const double* vals, int nparts, uint64_t k,
+                               uint64_t p, int mode, bkg_psolver** out);
+/* One part per process (rank), NCCL over NVLink.  local_row_offsets has
+ * row_end-row_begin+1 entries starting at 0; cols are GLOBAL indices.      */
+int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
+                            uint64_t row_end, const uint64_t* local_row_offsets,
+                            const uint64_t* cols, const double* vals, uint64_t k, uint64_t p,
+                            int mode, int rank, int nranks, const void* nccl_id,
+                            bkg_psolver** out);
+int bkg_psolver_destroy(bkg_psolver* s);
+/* virtual: global B (n*k); NCCL: this rank's rows.                         */
+int bkg_psolver_set_rhs(bkg_psolver* s, const double* b);
+int bkg_psolver_run(bkg_psolver* s, double tol, uint64_t max_iter, int record_history,
+                    double* final_norms /* nullable, k */, bkg_report* rep);
+int bkg_psolver_get_x(bkg_psolver* s, double* x);
+int bkg_psolver_history(bkg_psolver* s, double* history, uint64_t cap, uint64_t* rows);
+
 /* ---- problem generators (problems.hpp + frozen new generators) ---------- */
 /* kinds: 0 poisson2d constant, 1 poisson2d log-uniform(seed, contrast),
  * 2 lognormal 2D diffusion (seed), 3 3D 7-point, 4 3D 27-point.            */

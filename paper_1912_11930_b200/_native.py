@@ -99,6 +99,19 @@ SIGNATURES = [
     ("bkg_solver_profile", C.c_int, [_vp, C.c_uint64, _d]),
     ("bkg_solver_debug_first_step", C.c_int, [_vp, _d, _d]),
     ("bkg_solver_kernel_bytes", C.c_int, [_vp, _d]),
+    ("bkg_halo_plan", C.c_int, [C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_uint64, _u]),
+    ("bkg_nccl_unique_id", C.c_int, [C.c_void_p]),
+    ("bkg_psolver_create_virtual", C.c_int, [_vp, C.c_uint64, _u, _u, _d, C.c_int, C.c_uint64,
+                                             C.c_uint64, C.c_int, C.POINTER(_vp)]),
+    ("bkg_psolver_create_nccl", C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, _u, _u, _d,
+                                          C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int,
+                                          C.c_void_p, C.POINTER(_vp)]),
+    ("bkg_psolver_destroy", C.c_int, [_vp]),
+    ("bkg_psolver_set_rhs", C.c_int, [_vp, _d]),
+    ("bkg_psolver_run", C.c_int, [_vp, C.c_double, C.c_uint64, C.c_int, _d, C.POINTER(Report)]),
+    ("bkg_psolver_get_x", C.c_int, [_vp, _d]),
+    ("bkg_psolver_history", C.c_int, [_vp, _d, C.c_uint64, _u]),
     ("bkg_stencil_size", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, _u, _u]),
     ("bkg_stencil_fill", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                    C.c_double, _u, _u, _d]),

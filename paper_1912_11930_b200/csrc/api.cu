@@ -20,6 +20,7 @@
 #include "kernels_exact.cuh"
 #include "kernels_fast.cuh"
 #include "precond.cuh"
+#include "host.cuh"
 
 namespace bkg {
 
@@ -98,12 +99,6 @@ int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int
   return (int)std::min<int64_t>((int64_t)nb * c->sm_count, need);
 }
 
-// Reduction scratch (partials, group partials, tickets) owned by a context.
-struct Scratch {
-  double* partials;
-  double* gpart;
-  Ctrl* ctrl;
-};
 
 Scratch ctx_scratch(bkg_ctx* c, int grid, int entries) {
   const size_t need = (size_t)(grid + kMaxTicketGroups) * entries;
@@ -238,15 +233,6 @@ int dev_bsolve(bkg_ctx* c, int nblk, int p, const double* gamma, const double* d
   return 0;
 }
 
-template <class T>
-void h2d(bkg_ctx* c, T* dst, const T* src, size_t count) {
-  if (count) BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
-}
-template <class T>
-void d2h(bkg_ctx* c, T* dst, const T* src, size_t count) {
-  if (count) BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-}
-void sync(bkg_ctx* c) { BKG_CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
 
 __global__ void k_u64_to_i32(int64_t count, const uint64_t* __restrict__ src,
                              int32_t* __restrict__ dst) {

@@ -102,6 +102,9 @@ struct Ctrl {
 };
 
 constexpr int kMaxTicketGroups = 63;
+// Column sentinel for inactive CSR slots: local column indices may be
+// negative in the row-partitioned solver (ghost rows below the own block).
+constexpr int kNoCol = -2147483647 - 1;
 
 // Every iteration kernel returns immediately once the device stop flag is set
 // (null ctrl: standalone kernel call, never stopped).

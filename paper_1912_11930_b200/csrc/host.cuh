@@ -1,0 +1,49 @@
+// host.cuh — host-side helpers shared by api.cu (single device solver and
+// the C ABI) and psolver.cu (row-partitioned solver).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "fast_table.cuh"
+
+namespace bkg {
+
+void activate(bkg_ctx* c);
+int elem_grid(const bkg_ctx* c, int64_t total);
+void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void** args);
+void allow_smem(const void* fn, int bytes);
+int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
+bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
+void check_cfg(uint64_t k, uint64_t p, int mode);
+void dev_gram(bkg_ctx* c, int64_t n, int k, int p, bool global, const double* x, const double* y,
+              double* out, bool force_exact);
+void dev_spmm(bkg_ctx* c, const bkg_matrix* A, int k, const double* x, double* y, const Ctrl* ctrl,
+              bool force_exact);
+
+// Reduction scratch (partials, group partials, tickets) owned by a context.
+struct Scratch {
+  double* partials;
+  double* gpart;
+  Ctrl* ctrl;
+};
+
+template <class T>
+void h2d(bkg_ctx* c, T* dst, const T* src, size_t count) {
+  if (count)
+    BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+}
+template <class T>
+void d2h(bkg_ctx* c, T* dst, const T* src, size_t count) {
+  if (count)
+    BKG_CUDA_CHECK(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+}
+template <class T>
+void d2d(bkg_ctx* c, T* dst, const T* src, size_t count) {
+  if (count)
+    BKG_CUDA_CHECK(
+        cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+}
+inline void sync(bkg_ctx* c) { BKG_CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
+
+}  // namespace bkg

@@ -177,6 +177,12 @@ struct IterArgs {
   int hist_ring;
   int group;
   Ctrl* ctrl;
+  // Row-partitioned solver (psolver.cu): the last CTA only publishes this
+  // part's totals -- red1 = [alpha | rho_prev], red2 = [rho | ||R_s||^2] --
+  // and the p x p solves run after the cross-part allreduce.
+  int dist;
+  double* red1;
+  double* red2;
 };
 
 // Last-CTA epilogue shared by both numerics modes: norms[k] are the column
@@ -256,11 +262,11 @@ __device__ __forceinline__ void spmm_row(const IterArgs& a, int64_t beg, int64_t
     for (int u = 0; u < CH; ++u) {
       const bool on = i + u < end;
       v[u] = on ? __ldg(a.vals + i + u) : 0.0;
-      c[u] = on ? __ldg(a.cols + i + u) : -1;
+      c[u] = on ? __ldg(a.cols + i + u) : kNoCol;
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      if (c[u] >= 0) {
+      if (c[u] != kNoCol) {
         ld_nc<CPT>(x[u], a.P + (int64_t)c[u] * K + col0);
       } else {
 #pragma unroll
@@ -269,7 +275,7 @@ __device__ __forceinline__ void spmm_row(const IterArgs& a, int64_t beg, int64_t
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u)
-      if (c[u] >= 0) {
+      if (c[u] != kNoCol) {
 #pragma unroll
         for (int j = 0; j < CPT; ++j) q[j] = fma(v[u], x[u][j], q[j]);
       }
@@ -357,6 +363,10 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k1_spmm_gram
   double* ws = alpha + 3 * S::CS;
   gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, alpha);
   __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
+    return;
+  }
   const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
@@ -437,9 +447,16 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
   double* norms = beta_s + S::CS;
   double* ws = sm + S::RED + 3 * S::CS + K;
   gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, rho);
-  for (int c = threadIdx.x; c < K; c += kThreads)
-    norms[c] = sqrt(red[(c / CPT) * NACC + P * CPT + (c % CPT)]);
+  for (int c = threadIdx.x; c < K; c += kThreads) {
+    const double ss = red[(c / CPT) * NACC + P * CPT + (c % CPT)];
+    norms[c] = a.dist ? ss : sqrt(ss);
+  }
   __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red2[i] = rho[i];
+    for (int c = threadIdx.x; c < K; c += kThreads) a.red2[S::CS + c] = norms[c];
+    return;
+  }
   const int bad = cta_bsolve<P>(S::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
   if (threadIdx.x == 0) a.ctrl->xpending = 1;  // K3 still owes X += P lambda
   if (bad >= 0) {
@@ -539,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   }
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
-  if (!fin) gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, a.coef + S::CS);  // rho_prev
+  if (!fin) gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
   if (threadIdx.x == 0) a.ctrl->xpending = 0;  // every CTA has read it (we are last)
 }
 

@@ -87,13 +87,13 @@ __device__ void gather_gram_mma(const double* red, int off, double* blocks) {
 // column nt*8 + 2*(lane&3) + i of the lane's group), summed over the 8 row
 // lanes and square-rooted.
 template <int K, int P, bool GLOBAL, int NACC>
-__device__ void gather_norms_mma(const double* red, int off, double* norms) {
+__device__ void gather_norms_mma(const double* red, int off, double* norms, bool squares) {
   using L = MmaLayout<K, P, GLOBAL>;
   for (int c = threadIdx.x; c < K; c += kThreads) {
     const int g = c / P, cc = c % P, nt = cc >> 3, i = cc & 1, l4 = (cc & 7) >> 1;
     double s = 0.0;
     for (int r = 0; r < 8; ++r) s += red[(g * 32 + (r << 2) + l4) * NACC + off + nt * 2 + i];
-    norms[c] = sqrt(s);
+    norms[c] = squares ? s : sqrt(s);
   }
 }
 
@@ -172,8 +172,13 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
   double* norms = beta_s + S::CS;
   double* ws = sm + S::RED + 3 * S::CS + K;
   gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, rho);
-  gather_norms_mma<K, P, GLOBAL, NACC>(red, NG, norms);
+  gather_norms_mma<K, P, GLOBAL, NACC>(red, NG, norms, a.dist != 0);
   __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red2[i] = rho[i];
+    for (int c = threadIdx.x; c < K; c += kThreads) a.red2[S::CS + c] = norms[c];
+    return;
+  }
   const int bad = cta_bsolve<P>(L::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
   if (threadIdx.x == 0) a.ctrl->xpending = 1;
   if (bad >= 0) {
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   extern __shared__ double sm[];
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
-  if (!fin) gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, a.coef + S::CS);  // rho_prev
+  if (!fin) gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
   if (threadIdx.x == 0) a.ctrl->xpending = 0;
 }
 
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1_MINB) k1_tile(IterArgs a) {
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       v[u] = u < len ? __ldg(a.vals + b + u) : 0.0;
-      c[u] = u < len ? __ldg(a.cols + b + u) : -1;
+      c[u] = u < len ? __ldg(a.cols + b + u) : kNoCol;
     }
   };
   // FMAs of one chunk: inactive slots carry v = 0, x = 0.
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1_MINB) k1_tile(IterArgs a) {
     double x[CH][2];
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      if (c[u] >= 0) {
+      if (c[u] != kNoCol) {
         ld_nc<2>(x[u], Pc + (int64_t)c[u] * K);
       } else {
         x[u][0] = x[u][1] = 0.0;
@@ -468,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, BKG_K1_MINB) k1_tile(IterArgs a) {
   double* ws = alpha + 3 * S::CS;
   gather_gram_tile<K, P, W, GLOBAL, NACC>(red, alpha);
   __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
+    return;
+  }
   const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }

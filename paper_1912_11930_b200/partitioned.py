@@ -1,0 +1,131 @@
+"""Row-partitioned Block-CG (multi-GPU path) over bkg_psolver_*.
+
+The rows of A are split into contiguous blocks; each block ("part") owns its
+rows of X, R, Q and a ghost-extended P.  Two transports share one code path:
+
+* ``PartitionedSolver.virtual(a, cfg, nparts)`` — all parts on this process's
+  device (halo = device copies, allreduce = fixed-order sum kernel): the
+  single-GPU emulation of ``nparts`` ranks used by the tests;
+* ``PartitionedSolver.nccl(...)`` — one part per process (torchrun rank), halo
+  with ncclSend/ncclRecv over NVLink, ncclAllReduce of the Gram partials.
+
+``halo_plan`` / ``need_range`` are the pure host logic (no GPU needed).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .blockkrylov import Context, SparseMatrix, SubalgebraConfig, _check, _dp, _up, default_context
+
+
+def row_blocks(n: int, nparts: int) -> List[int]:
+    """Contiguous near-equal row blocks [b[r], b[r+1]) (same split as the C ABI)."""
+    return [n * r // nparts for r in range(nparts + 1)]
+
+
+def local_csr(a: SparseMatrix, r0: int, r1: int):
+    """Rows [r0, r1) of A: (local row offsets from 0, global columns, values)."""
+    off = a.row_offsets()
+    s, e = int(off[r0]), int(off[r1])
+    lrp = (off[r0:r1 + 1] - off[r0]).astype(np.uint64)
+    return lrp, a.col_indices()[s:e].copy(), a.values()[s:e].copy()
+
+
+def need_range(r0: int, r1: int, cols: np.ndarray) -> Tuple[int, int]:
+    """Operand rows a part touches: [min(r0, min col), max(r1, max col + 1))."""
+    if cols.size == 0:
+        return r0, r1
+    return min(r0, int(cols.min())), max(r1, int(cols.max()) + 1)
+
+
+def halo_plan(row_begin, need_lo, need_hi) -> List[Tuple[int, int, int, int]]:
+    """(dst part, src part, first global row, rows) copies (bkg_halo_plan)."""
+    nparts = len(need_lo)
+    rb = np.ascontiguousarray(row_begin, dtype=np.int64)
+    lo = np.ascontiguousarray(need_lo, dtype=np.int64)
+    hi = np.ascontiguousarray(need_hi, dtype=np.int64)
+    cap = nparts * nparts
+    out = np.zeros(4 * max(cap, 1), dtype=np.int64)
+    cnt = C.c_uint64()
+    p64 = C.POINTER(C.c_int64)
+    _check(N.lib().bkg_halo_plan(nparts, rb.ctypes.data_as(p64), lo.ctypes.data_as(p64),
+                                 hi.ctypes.data_as(p64), out.ctypes.data_as(p64), cap,
+                                 C.byref(cnt)))
+    return [tuple(int(v) for v in out[4 * i:4 * i + 4]) for i in range(cnt.value)]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(N.lib().bkg_nccl_unique_id(buf))
+    return buf.raw
+
+
+class PartitionedSolver:
+    def __init__(self, handle, ctx: Context, n: int, k: int, rows: Tuple[int, int], virtual: bool):
+        self.handle, self.ctx, self.n, self.k = handle, ctx, n, k
+        self.rows = rows
+        self.is_virtual = virtual
+
+    @staticmethod
+    def virtual(a: SparseMatrix, cfg: SubalgebraConfig, nparts: int,
+                ctx: Optional[Context] = None) -> "PartitionedSolver":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(N.lib().bkg_psolver_create_virtual(ctx.handle, a.n(), _up(a.row_offsets()),
+                                                  _up(a.col_indices()), _dp(a.values()), nparts,
+                                                  cfg.k, cfg.p, cfg._mode_code, C.byref(h)))
+        return PartitionedSolver(h, ctx, a.n(), cfg.k, (0, a.n()), True)
+
+    @staticmethod
+    def nccl(n_global: int, r0: int, r1: int, lrowptr, cols, vals, cfg: SubalgebraConfig,
+             rank: int, nranks: int, nccl_id: bytes,
+             ctx: Optional[Context] = None) -> "PartitionedSolver":
+        ctx = ctx or default_context()
+        lrowptr = np.ascontiguousarray(lrowptr, dtype=np.uint64)
+        cols = np.ascontiguousarray(cols, dtype=np.uint64)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        h = C.c_void_p()
+        idb = C.create_string_buffer(nccl_id, 128)
+        _check(N.lib().bkg_psolver_create_nccl(ctx.handle, n_global, r0, r1, _up(lrowptr),
+                                               _up(cols), _dp(vals), cfg.k, cfg.p,
+                                               cfg._mode_code, rank, nranks, idb, C.byref(h)))
+        return PartitionedSolver(h, ctx, n_global, cfg.k, (r0, r1), False)
+
+    def set_rhs(self, b: np.ndarray) -> None:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        _check(N.lib().bkg_psolver_set_rhs(self.handle, _dp(b)))
+
+    def run(self, tol: float = 1e-8, max_iter: int = 0, record_history: bool = False,
+            final_norms: bool = False):
+        rep = N.Report()
+        fin = np.zeros(self.k)
+        _check(N.lib().bkg_psolver_run(self.handle, tol, max_iter, int(record_history),
+                                       _dp(fin) if final_norms else None, C.byref(rep)))
+        return rep, fin
+
+    def x(self) -> np.ndarray:
+        rows = self.rows[1] - self.rows[0]
+        out = np.empty((rows, self.k))
+        _check(N.lib().bkg_psolver_get_x(self.handle, _dp(out)))
+        return out
+
+    def history(self, cap: int) -> np.ndarray:
+        out = np.empty((max(cap, 1), self.k))
+        rows = C.c_uint64()
+        _check(N.lib().bkg_psolver_history(self.handle, _dp(out), cap, C.byref(rows)))
+        return out[: min(cap, rows.value)]
+
+    def close(self) -> None:
+        if self.handle:
+            N.lib().bkg_psolver_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,97 @@
+"""Row-partitioned solver on one B200: `nparts` virtual parts (the single-GPU
+emulation of nparts ranks: halo copies + fixed-order allreduce), and the NCCL
+transport with one rank.  Checked against the reference fixtures / oracle
+with the north_star bars, and against the unpartitioned solver."""
+import numpy as np
+import pytest
+
+import golden_io
+import paper_1912_11930_b200 as bk
+from cases import BY_NAME, build_inputs
+from paper_1912_11930_b200.partitioned import PartitionedSolver, local_csr, nccl_unique_id
+
+pytestmark = pytest.mark.gpu
+
+
+class Gen:
+    def stencil(self, kind, nx, ny, nz=1, seed=0, contrast=2.0):
+        a = bk.stencil(kind, nx, ny, nz, seed=seed, contrast=contrast)
+        return a.row_offsets(), a.col_indices(), a.values()
+
+    normal_block_rhs = staticmethod(bk.normal_block_rhs)
+    random_block_rhs = staticmethod(bk.random_block_rhs)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = bk.Context(0, "fast")
+    yield c
+    c.close()
+
+
+def inputs(name):
+    case = BY_NAME[name]
+    csr, b, _ = build_inputs(case, Gen())
+    a = bk.SparseMatrix(len(csr[0]) - 1, *csr, validate=False)
+    return case, a, b
+
+
+@pytest.mark.parametrize("name", ["c2_24", "c4_14_classical", "c4_14_hybrid4", "c4_14_global4",
+                                  "c5_16", "c1_classical", "c1_parallel"])
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4])
+def test_virtual_parts_meet_parity_bars(ctx, port, name, nparts):
+    case, a, b = inputs(name)
+    g = golden_io.load(name)
+    cfg = bk.SubalgebraConfig(case.k, case.p, case.mode)
+    s = PartitionedSolver.virtual(a, cfg, nparts, ctx)
+    s.set_rhs(b)
+    rep, fin = s.run(case.tol, case.max_iter, record_history=True, final_norms=True)
+    hist = s.history(rep.history_rows)
+    x = s.x()
+    s.close()
+    m = g["meta"]
+    assert rep.converged == m["converged"]
+    assert abs(rep.iterations - m["iterations"]) <= 1
+    rows = min(len(hist), len(g["history"]))
+    drift = np.max(np.abs(hist[:rows] - g["history"][:rows]) / g["history"][:rows])
+    assert drift <= 1e-9, drift
+    ref = port.bcg_solve((a.row_offsets(), a.col_indices(), a.values()), b, case.p, case.glob,
+                         tol=case.tol, max_iter=case.max_iter, record_history=False)
+    xs = np.linalg.norm(x - ref.x, axis=0) / np.linalg.norm(ref.x, axis=0)
+    assert np.max(xs) <= 1e-8
+    np.testing.assert_allclose(fin, ref.final_norms, rtol=1e-6, atol=1e-12)
+    assert rep.flops_bdot == m["flops_bdot"] and rep.flops_bop == m["flops_bop"]
+
+
+def test_nccl_single_rank_matches_virtual(ctx):
+    case, a, b = inputs("c2_24")
+    cfg = bk.SubalgebraConfig(case.k, case.p, case.mode)
+    lrp, cols, vals = local_csr(a, 0, a.n())
+    s = PartitionedSolver.nccl(a.n(), 0, a.n(), lrp, cols, vals, cfg, 0, 1, nccl_unique_id(), ctx)
+    s.set_rhs(b)
+    rep, _ = s.run(case.tol, case.max_iter, record_history=True)
+    xn, hn = s.x(), s.history(rep.history_rows)
+    s.close()
+    v = PartitionedSolver.virtual(a, cfg, 1, ctx)
+    v.set_rhs(b)
+    rep1, _ = v.run(case.tol, case.max_iter, record_history=True)
+    assert rep.iterations == rep1.iterations
+    assert hn.tobytes() == v.history(rep1.history_rows).tobytes()  # same kernels, same order
+    assert xn.tobytes() == v.x().tobytes()
+    v.close()
+
+
+def test_partitioned_breakdown_and_maxiter(ctx):
+    case, a, b = inputs("c2_24")
+    b = b.copy()
+    b[:, 5] = b[:, 1]  # duplicate column inside p-group 0 -> singular alpha block 0
+    s = PartitionedSolver.virtual(a, bk.SubalgebraConfig(32, 8), 3, ctx)
+    s.set_rhs(b)
+    rep, _ = s.run(1e-8, 0)
+    assert rep.breakdown == 1 and rep.breakdown_iteration == 1 and rep.breakdown_block == 0
+    s.close()
+    s = PartitionedSolver.virtual(a, bk.SubalgebraConfig(32, 8), 2, ctx)
+    s.set_rhs(bk.normal_block_rhs(a.n(), 32, 7))
+    rep, _ = s.run(1e-30, 5)
+    assert rep.iterations == 5 and not rep.converged
+    s.close()
