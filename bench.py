@@ -20,9 +20,10 @@ cpu_baseline: the reference CPU solver (oracle/_ref, built from
          cores, on a bounded sample of the same workload.
 --impl reference: the reference CPU implementation alone (all host threads).
 
-Multi-GPU (torchrun, N > 1): every rank solves its own replica of the
-workload (weak scaling, "replicas only" until the row-partitioned solver
-lands); value = sum over ranks / max-over-ranks time.
+Multi-GPU (torchrun, N > 1): the same C2 system, rows split into N
+contiguous slabs (one per rank), P halo via ncclSend/Recv and the Gram
+partials via ncclAllReduce (paper_1912_11930_b200/partitioned.py); strong
+scaling, value = k * iterations / max-over-ranks solve time.
 """
 from __future__ import annotations
 
@@ -262,6 +263,9 @@ def run_ours(args):
             ms = float(t.item())
         return ms, out
 
+    if dist:
+        return run_partitioned(args, bk, ctx, stream, a, b, cfg, timed, rank, ws, local)
+
     # ---------------- value: resident inputs -------------------------------
     solver = bk.DeviceSolver(a, cfg, ctx)
     solver.set_rhs(b)
@@ -300,12 +304,13 @@ def run_ours(args):
     pin_col[...] = a.col_indices()
     pin_val = torch.empty(nnz, dtype=torch.float64, pin_memory=True).numpy()
     pin_val[...] = a.values()
+    pin_x = torch.empty((n, k), dtype=torch.float64, pin_memory=True).numpy()
     m = bk.Preconditioner.identity(n)
     opts = bk.SolveOptions(tol=tol, max_iter=max_iter)
 
     def e2e_step():
         am = bk.SparseMatrix(n, pin_off, pin_col, pin_val, validate=False)
-        res = bk.bcg_solve(am, pin_b, m, cfg, opts, ctx=ctx)
+        res = bk.bcg_solve(am, pin_b, m, cfg, opts, ctx=ctx, out=pin_x)
         am.release_device()
         return res.report.iterations
 
@@ -354,6 +359,68 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         tdist.destroy_process_group()
+    return 0
+
+
+def run_partitioned(args, bk, ctx, stream, a, b, cfg, timed, rank, ws, local):
+    """N > 1: one C2 system, rows split into N contiguous slabs (z-slabs of the
+    lexicographic grid), one slab per rank; halo of P with ncclSend/Recv,
+    Gram partials with ncclAllReduce (paper_1912_11930_b200/partitioned.py).
+    Strong scaling: value = k * iterations / (max-over-ranks solve time)."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1912_11930_b200.partitioned import (PartitionedSolver, local_csr, nccl_unique_id,
+                                                   row_blocks)
+    kind, nx, ny, nz, k, p, mode, rhs, tol, max_iter, desc = CONFIGS[args.config]
+    n, nnz = a.n(), a.nnz()
+    rb = row_blocks(n, ws)
+    r0, r1 = rb[rank], rb[rank + 1]
+    lrp, cols, vals = local_csr(a, r0, r1)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0)
+    nid = obj[0]
+    s = PartitionedSolver.nccl(n, r0, r1, lrp, cols, vals, cfg, rank, ws, nid, ctx)
+    s.set_rhs(b[r0:r1])
+    for _ in range(args.warmup):
+        s.run(tol, max_iter)
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clocks:
+        ms, reps = timed(lambda: s.run(tol, max_iter)[0], args.steps)
+    launches = ctx.launch_count() - launches0
+    its = [int(r.iterations) for r in reps]
+    value = k * sum(its) / (ms * 1e-3)
+    s.close()
+
+    # e2e: host slab in (CSR + B), X slab out, through the partitioned API
+    def e2e_step():
+        t = PartitionedSolver.nccl(n, r0, r1, lrp, cols, vals, cfg, rank, ws, nid, ctx)
+        t.set_rhs(b[r0:r1])
+        rep, _ = t.run(tol, max_iter)
+        t.x()
+        t.close()
+        return int(rep.iterations)
+
+    e2e_ms, e2e_its = timed(e2e_step, 1)
+    nloc = r1 - r0
+    h2d = 8 * (nloc + 1) + 16 * len(vals) + 8 * nloc * k
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, DESIGN.md §Inputs)",
+            "config": {"workload": desc, "n": n, "nnz": nnz, "k": k, "p": p, "mode": mode,
+                       "tol": tol, "iterations_per_solve": its[0],
+                       "parallelism": f"row-partitioned x{ws} (z-slabs), NCCL halo + allreduce",
+                       "l2": "inputs larger than L2 per rank"},
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": k * sum(e2e_its) / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * nloc * k},
+            "clocks": clocks.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
     return 0
 
 

@@ -544,8 +544,12 @@ class SolveResult:
     report: SolveReport
 
 
-def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None) -> SolveResult:
-    """bcg_solve(a, b, [x0,] m, cfg, opts=SolveOptions()) — solver.hpp:106-216."""
+def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None,
+              out: Optional[np.ndarray] = None) -> SolveResult:
+    """bcg_solve(a, b, [x0,] m, cfg, opts=SolveOptions()) — solver.hpp:106-216.
+
+    ``out`` (optional, (n, k) float64 C-order, e.g. pinned host memory) receives
+    X instead of a freshly allocated array."""
     if len(args) and isinstance(args[0], np.ndarray):
         x0, rest = args[0], args[1:]
     else:
@@ -570,7 +574,12 @@ def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None) -> Solve
         raise ConfigError("bcg_solve: tol must be positive")
     ctx = ctx or default_context()
     n, k = b.shape
-    x = np.empty_like(b)
+    if out is not None:
+        if out.shape != b.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise DimensionError("bcg_solve: out must be a C-contiguous float64 (n x k) array")
+        x = out
+    else:
+        x = np.empty_like(b)
     max_iter = opts.max_iter or 10 * n
     cap = (max_iter + 1) if opts.record_history else 0
     cap = min(cap, max(1, (1 << 28) // max(k, 1)))

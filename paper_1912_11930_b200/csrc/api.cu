@@ -113,7 +113,8 @@ Scratch ctx_scratch(bkg_ctx* c, int grid, int entries) {
 
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t) {
   if (c->numerics != BKG_NUMERICS_FAST) return false;
-  return fast_lookup(k, p, global, t);
+  FastTable tmp;
+  return fast_lookup(k, p, global, t ? t : &tmp);
 }
 
 void check_cfg(uint64_t k, uint64_t p, int mode) {
@@ -233,6 +234,28 @@ int dev_bsolve(bkg_ctx* c, int nblk, int p, const double* gamma, const double* d
   return 0;
 }
 
+
+// CSR upload: structural checks of sparse_matrix.hpp:96-105 (bit 1: offsets
+// decrease, 2: column out of range, 4: columns not strictly ascending) and
+// the size_t -> int32 column conversion, one thread per row.
+__global__ void k_csr_check_convert(int64_t n, const int64_t* __restrict__ rowptr,
+                                    const uint64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                    int* err) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = rowptr[r], e = rowptr[r + 1];
+    int bad = e < b ? 1 : 0;
+    uint64_t prev = 0;
+    for (int64_t i = b; i < e; ++i) {
+      const uint64_t c = src[i];
+      if (c >= (uint64_t)n) bad |= 2;
+      if (i > b && c <= prev) bad |= 4;
+      prev = c;
+      dst[i] = (int32_t)c;
+    }
+    if (bad) atomicOr(err, bad);
+  }
+}
 
 __global__ void k_u64_to_i32(int64_t count, const uint64_t* __restrict__ src,
                              int32_t* __restrict__ dst) {
@@ -598,6 +621,7 @@ int bkg_ctx_destroy(bkg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->solver_cache_free) ctx->solver_cache_free(ctx->solver_cache);
     ctx->scratch.release();
     ctx->ctrl.release();
     cudaStreamDestroy(ctx->stream);
@@ -629,20 +653,14 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
                       const double* vals, bkg_matrix** out) {
   return guard([&] {
     *out = nullptr;
-    // structural checks of sparse_matrix.hpp:89-105 (value symmetry is the
-    // host SparseMatrix constructor's job)
+    // structural checks of sparse_matrix.hpp:89-105 run on the device during
+    // the upload (k_csr_check_convert); value symmetry is the host
+    // SparseMatrix constructor's job.
     BKG_REQUIRE(n > 0, BKG_CONFIG, "sparse matrix: dimension must be positive");
     BKG_REQUIRE(n < (1ull << 31), BKG_CONFIG, "sparse matrix: n must be < 2^31 on device");
     BKG_REQUIRE(off[0] == 0, BKG_CONFIG, "sparse matrix: offsets inconsistent with stored entries");
     const uint64_t nnz = off[n];
-    for (uint64_t r = 0; r < n; ++r) {
-      BKG_REQUIRE(off[r] <= off[r + 1], BKG_CONFIG, "sparse matrix: row_offsets must be non-decreasing");
-      for (uint64_t i = off[r]; i < off[r + 1]; ++i) {
-        BKG_REQUIRE(cols[i] < n, BKG_CONFIG, "sparse matrix: column index out of range");
-        BKG_REQUIRE(i == off[r] || cols[i] > cols[i - 1], BKG_CONFIG,
-                    "sparse matrix: columns must be strictly ascending per row");
-      }
-    }
+    BKG_REQUIRE(nnz < (1ull << 40), BKG_CONFIG, "sparse matrix: offsets inconsistent with stored entries");
     activate(ctx);
     auto* m = new bkg_matrix();
     m->ctx = ctx;
@@ -654,17 +672,23 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
       m->vals.alloc(std::max<uint64_t>(nnz, 1));
       h2d(ctx, reinterpret_cast<uint64_t*>(m->rowptr.ptr), off, n + 1);
       h2d(ctx, m->vals.ptr, vals, nnz);
-      if (nnz) {
-        DevBuf<uint64_t> tmp(nnz);
-        h2d(ctx, tmp.ptr, cols, nnz);
-        int64_t cnt = (int64_t)nnz;
-        const uint64_t* s = tmp.ptr;
-        int32_t* d = m->cols.ptr;
-        void* args[] = {&cnt, &s, &d};
-        launch(ctx, (const void*)&k_u64_to_i32, elem_grid(ctx, cnt), 256, 0, args);
-        sync(ctx);
-      }
+      ctx->upload_tmp.ensure(std::max<uint64_t>(nnz, 1) * sizeof(uint64_t) + 64);
+      uint64_t* tmp = reinterpret_cast<uint64_t*>(ctx->upload_tmp.ptr);
+      int* err = reinterpret_cast<int*>(ctx->upload_tmp.ptr + std::max<uint64_t>(nnz, 1) * 8);
+      BKG_CUDA_CHECK(cudaMemsetAsync(err, 0, sizeof(int), ctx->stream));
+      h2d(ctx, tmp, cols, nnz);
+      int64_t nn = (int64_t)n;
+      const int64_t* rp = m->rowptr.ptr;
+      const uint64_t* src = tmp;
+      int32_t* dst = m->cols.ptr;
+      void* args[] = {&nn, &rp, &src, &dst, &err};
+      launch(ctx, (const void*)&k_csr_check_convert, elem_grid(ctx, nn), 256, 0, args);
+      int herr = 0;
+      d2h(ctx, &herr, err, 1);
       sync(ctx);
+      BKG_REQUIRE(!(herr & 1), BKG_CONFIG, "sparse matrix: row_offsets must be non-decreasing");
+      BKG_REQUIRE(!(herr & 2), BKG_CONFIG, "sparse matrix: column index out of range");
+      BKG_REQUIRE(!(herr & 4), BKG_CONFIG, "sparse matrix: columns must be strictly ascending per row");
     } catch (...) {
       delete m;
       throw;
@@ -957,11 +981,24 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
                     opts->precond == BKG_PRECOND_ILU0,
                 BKG_CONFIG, "unknown preconditioner");
     activate(ctx);
-    bkg_solver s;
-    s.precond = opts->precond;
-    BKG_REQUIRE(s.precond == BKG_PRECOND_IDENTITY, BKG_CONFIG,
+    BKG_REQUIRE(opts->precond == BKG_PRECOND_IDENTITY, BKG_CONFIG,
                 "bcg_solve: only the identity preconditioner runs in the device loop");
-    s.init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL);
+    // Reuse the previous call's device workspace when the shape matches
+    // (repeated drop-in solves do not re-allocate ~5 block vectors each).
+    bkg_solver* cached = static_cast<bkg_solver*>(ctx->solver_cache);
+    const bool glob = mode == BKG_GLOBAL && p != k;
+    if (!cached || cached->n != (int64_t)a->n || cached->k != (int)k || cached->p != (int)p ||
+        cached->global != glob || cached->fast != use_fast(ctx, (int)k, (int)p, glob, nullptr)) {
+      if (ctx->solver_cache_free) ctx->solver_cache_free(ctx->solver_cache);
+      ctx->solver_cache = nullptr;
+      cached = new bkg_solver();
+      ctx->solver_cache = cached;
+      ctx->solver_cache_free = [](void* q) { delete static_cast<bkg_solver*>(q); };
+      cached->init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL);
+    }
+    bkg_solver& s = *cached;
+    s.A = a;
+    s.precond = opts->precond;
     h2d(ctx, s.B.ptr, b, (size_t)a->n * k);
     s.have_b = true;
     s.run(x0, opts->tol, opts->max_iter, opts->record_history != 0, opts->on_iterate, opts->user,

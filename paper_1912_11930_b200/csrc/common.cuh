@@ -123,6 +123,10 @@ struct bkg_ctx {
   // scratch (reused across calls on this ctx)
   bkg::DevBuf<double> scratch;
   bkg::DevBuf<char> ctrl;  // one bkg::Ctrl for standalone kernels
+  bkg::DevBuf<char> upload_tmp;  // staging for size_t column uploads
+  // device workspace of the last bkg_solve call (reused when shapes match)
+  void* solver_cache = nullptr;
+  void (*solver_cache_free)(void*) = nullptr;
 };
 
 struct bkg_matrix {

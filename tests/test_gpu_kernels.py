@@ -314,3 +314,15 @@ def test_kernels_finite(ctx):
     z = bk.bop(a, x, ctx=ctx)
     s = bk.bsolve(bk.bdot(x, x, c, ctx=ctx), g, ctx=ctx)
     assert np.all(np.isfinite(x)) and np.all(np.isfinite(z)) and np.all(np.isfinite(s.data))
+
+
+def test_matrix_upload_validates_structure_on_device(ctx):
+    # sparse_matrix.hpp:96-105 structural checks, enforced by bkg_matrix_create
+    bad = [([0, 2, 1], [0, 1, 0], 3),        # offsets decrease
+           ([0, 1, 2], [0, 5], 2),            # column out of range
+           ([0, 2, 3], [1, 0, 1], 3)]         # columns not ascending
+    for off, cols, nnz in bad:
+        a = bk.SparseMatrix(len(off) - 1, np.array(off, np.uint64)[: len(off)],
+                            np.array(cols, np.uint64), np.ones(len(cols)), validate=False)
+        with pytest.raises(bk.ConfigError):
+            bk.bop(a, np.ones((a.n(), 2)), ctx=ctx)
