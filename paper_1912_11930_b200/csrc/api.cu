@@ -85,8 +85,11 @@ void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void**
   c->launches++;
 }
 
+// Opt in to > 48 KB of shared memory when static + dynamic exceed it.
 void allow_smem(const void* fn, int bytes) {
-  if (bytes > 48 * 1024)
+  cudaFuncAttributes fa;
+  BKG_CUDA_CHECK(cudaFuncGetAttributes(&fa, fn));
+  if (bytes + (int)fa.sharedSizeBytes > 48 * 1024)
     BKG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
