@@ -93,6 +93,11 @@ int bkg_column_norms(bkg_ctx* ctx, uint64_t n, uint64_t k, const double* x, doub
 int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k,
                       const double* r, double* z, uint64_t* flops_precond);
 
+/* Factor / validate a preconditioner for `a` on the device (Jacobi: diagonal
+ * > 0, preconditioners.hpp:48-59; ILU(0): ilu0_factor :153-196).  On
+ * BKG_FACTORIZATION *bad_row is the FactorizationError row.                */
+int bkg_precond_setup(bkg_ctx* ctx, bkg_matrix* a, int precond, int64_t* bad_row);
+
 /* ---- solver (solver.hpp:21-216) ----------------------------------------- */
 /* SolveReport (solver.hpp:48-59) flattened.  defect_history is returned via
  * the caller's buffer (history_cap rows of k doubles).                      */

@@ -88,6 +88,7 @@ SIGNATURES = [
     ("bkg_bsolve", C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int, _d, _d, _d, _u]),
     ("bkg_column_norms", C.c_int, [_vp, C.c_uint64, C.c_uint64, _d, _d]),
     ("bkg_precond_apply", C.c_int, [_vp, _vp, C.c_int, C.c_uint64, _d, _d, _u]),
+    ("bkg_precond_setup", C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_int64)]),
     ("bkg_solve", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_int, _d, _d,
                             C.POINTER(SolveOptions), _d, _d, C.c_uint64, _d, C.POINTER(Report)]),
     ("bkg_solver_create", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(_vp)]),

@@ -494,8 +494,17 @@ class Preconditioner:
         return z
 
 
-def ilu0_factor(a: SparseMatrix) -> Preconditioner:
-    """ILU(0) (preconditioners.hpp:153-196); factored on the device."""
+def _precond_setup(a: SparseMatrix, kind: str, ctx: Optional[Context] = None) -> None:
+    ctx = ctx or default_context()
+    bad = C.c_int64(-1)
+    st = N.lib().bkg_precond_setup(ctx.handle, a.device(ctx), _PREC[kind], C.byref(bad))
+    _check(st, row=int(bad.value))
+
+
+def ilu0_factor(a: SparseMatrix, ctx: Optional[Context] = None) -> Preconditioner:
+    """ILU(0) (preconditioners.hpp:153-196), factored on the device now (so a
+    zero pivot raises FactorizationError here, as in the reference)."""
+    _precond_setup(a, ILU0, ctx)
     return Preconditioner(ILU0, a.n(), a)
 
 

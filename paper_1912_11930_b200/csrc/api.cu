@@ -301,16 +301,20 @@ struct bkg_solver {
     if (h_ring) cudaFreeHost(h_ring);
   }
 
-  void init(bkg_ctx* c, const bkg_matrix* a, int kk, int pp, bool gl) {
+  void init(bkg_ctx* c, const bkg_matrix* a, int kk, int pp, bool gl,
+            int pc = BKG_PRECOND_IDENTITY) {
     ctx = c;
     A = a;
     n = (int64_t)a->n;
     k = kk;
     p = pp;
+    precond = pc;
     global = gl && pp != kk;  // global with p = k is classical (test_kernels.cpp:131-140)
     nblk = global ? 1 : k / p;
     cs = nblk * p * p;
-    fast = use_fast(c, k, p, global, &ft);
+    // the fused fast loop is M = I; preconditioned solves run the unfused
+    // (reference-order) kernel sequence with Z = M^-1 R on device
+    fast = use_fast(c, k, p, global, &ft) && precond == BKG_PRECOND_IDENTITY;
     const size_t nk = (size_t)n * k;
     B.alloc(nk);
     X.alloc(nk);
@@ -391,13 +395,7 @@ struct bkg_solver {
     }
     dev_baxpy(ctx, n, k, p, global, X.ptr, P, cf, cc, true);                  // X += P lambda
     dev_baxpy(ctx, n, k, p, global, R.ptr, Q.ptr, cf + 5 * cs, cc, true);     // R -= Q lambda
-    {
-      int64_t tot = n * k;
-      const double* src = R.ptr;
-      double* dst = Z;
-      void* args[] = {&cc, &tot, &src, &dst};
-      launch(ctx, (const void*)&k_copy, elem_grid(ctx, tot), 256, 0, args);  // Z = M^-1 R
-    }
+    precond_apply_dev(ctx, const_cast<bkg_matrix*>(A), precond, k, R.ptr, Z, cc);  // Z = M^-1 R
     dev_chain(ctx, false, n, k, p, global, Z, R.ptr, cf + 3 * cs, cc);        // rho
     dev_chain(ctx, true, n, k, 1, false, R.ptr, R.ptr, norms.ptr, cc);        // ||R_s||
     if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
@@ -423,6 +421,7 @@ struct bkg_solver {
   bool setup(const double* x0_host, double tol, uint64_t max_iter, bool record,
              bkg_report* rep, std::vector<double>* limits_host, bool* x0_nonzero) {
     const size_t nk = (size_t)n * k;
+    precond_ready(ctx, const_cast<bkg_matrix*>(A), precond);  // FactorizationError surfaces here
     bool x0_zero = true;
     if (x0_host) {
       for (size_t i = 0; i < nk && x0_zero; ++i) x0_zero = x0_host[i] == 0.0;
@@ -469,8 +468,12 @@ struct bkg_solver {
     h2d(ctx, reinterpret_cast<char*>(dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
     P = Pb.ptr;
     Z = Zb.ptr;
-    if (!conv) {  // P^1 = M^-1 R^0 (identity: copy, solver.hpp:152-155)
-      BKG_CUDA_CHECK(cudaMemcpyAsync(P, R.ptr, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (!conv) {  // P^1 = M^-1 R^0 (solver.hpp:152-155)
+      if (precond == BKG_PRECOND_IDENTITY)
+        BKG_CUDA_CHECK(cudaMemcpyAsync(P, R.ptr, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        rep->flops_precond +=
+            precond_apply_dev(ctx, const_cast<bkg_matrix*>(A), precond, k, R.ptr, P, nullptr);
       // fast mode: K3 of iteration i produces rho_prev for iteration i+1;
       // the first one, <<P^1, R^0>>, comes from a standalone Gram launch.
       if (fast) dev_gram(ctx, n, k, p, global, P, R.ptr, coef.ptr + cs);
@@ -552,6 +555,8 @@ struct bkg_solver {
       bdots += h.stage == 1 ? 2 : 3;
       baxpys += h.stage == 1 ? 0 : 2;
     }
+    const uint64_t applies = h.iterations + ((h.breakdown && h.stage == 2) ? 1 : 0);
+    rep->flops_precond += applies * precond_flops(A, precond, k);
     (void)conv0;
     rep->flops_bdot += bdots * bdot1;
     rep->flops_baxpy += baxpys * bdot1;
@@ -835,6 +840,17 @@ int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k
   });
 }
 
+int bkg_precond_setup(bkg_ctx* ctx, bkg_matrix* a, int precond, int64_t* bad_row) {
+  const int st = guard([&] {
+    BKG_REQUIRE(precond >= BKG_PRECOND_IDENTITY && precond <= BKG_PRECOND_ILU0, BKG_CONFIG,
+                "unknown preconditioner");
+    activate(ctx);
+    precond_ready(ctx, a, precond);
+  });
+  if (bad_row) *bad_row = st == BKG_FACTORIZATION ? a->bad_row : -1;
+  return st;
+}
+
 int bkg_solver_create(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
                       bkg_solver** out) {
   return guard([&] {
@@ -984,20 +1000,20 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
                     opts->precond == BKG_PRECOND_ILU0,
                 BKG_CONFIG, "unknown preconditioner");
     activate(ctx);
-    BKG_REQUIRE(opts->precond == BKG_PRECOND_IDENTITY, BKG_CONFIG,
-                "bcg_solve: only the identity preconditioner runs in the device loop");
     // Reuse the previous call's device workspace when the shape matches
     // (repeated drop-in solves do not re-allocate ~5 block vectors each).
     bkg_solver* cached = static_cast<bkg_solver*>(ctx->solver_cache);
     const bool glob = mode == BKG_GLOBAL && p != k;
     if (!cached || cached->n != (int64_t)a->n || cached->k != (int)k || cached->p != (int)p ||
-        cached->global != glob || cached->fast != use_fast(ctx, (int)k, (int)p, glob, nullptr)) {
+        cached->global != glob || cached->precond != opts->precond ||
+        cached->fast != (use_fast(ctx, (int)k, (int)p, glob, nullptr) &&
+                         opts->precond == BKG_PRECOND_IDENTITY)) {
       if (ctx->solver_cache_free) ctx->solver_cache_free(ctx->solver_cache);
       ctx->solver_cache = nullptr;
       cached = new bkg_solver();
       ctx->solver_cache = cached;
       ctx->solver_cache_free = [](void* q) { delete static_cast<bkg_solver*>(q); };
-      cached->init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL);
+      cached->init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL, opts->precond);
     }
     bkg_solver& s = *cached;
     s.A = a;

@@ -139,6 +139,9 @@ struct bkg_matrix {
   bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)
   bkg::DevBuf<double> lu;        // ILU(0) factors on A's pattern
   int precond_ready = -1;        // kind whose factors are resident
+  bkg::DevBuf<int64_t> diag_pos;  // ILU: position of A(r,r) in the CSR
+  uint64_t ilu_offdiag = 0;       // ILU: stored off-diagonal entries
+  int64_t bad_row = -1;           // row of the last FactorizationError
   // ILU level schedule
   bkg::DevBuf<int32_t> level_rows;  // rows ordered by level
   std::vector<int64_t> level_ptr_fwd, level_ptr_bwd;

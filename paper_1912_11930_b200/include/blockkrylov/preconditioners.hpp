@@ -56,6 +56,20 @@ class Preconditioner {
     return m;
   }
 
+  /// ILU(0) factored on the device now (FactorizationError on a zero or
+  /// missing pivot, preconditioners.hpp:153-196).
+  static Preconditioner ilu0(const SparseMatrix& a) {
+    int64_t bad = -1;
+    const int st = bkg_precond_setup(gpu::context(), const_cast<bkg_matrix*>(a.device()),
+                                     BKG_PRECOND_ILU0, &bad);
+    detail::check(st, bad < 0 ? 0 : static_cast<std::size_t>(bad));
+    Preconditioner m;
+    m.kind_ = PreconditionerKind::ilu0;
+    m.n_ = a.n();
+    m.a_ = &a;
+    return m;
+  }
+
   PreconditionerKind kind() const noexcept { return kind_; }
   std::size_t n() const noexcept { return n_; }
   const SparseMatrix* matrix() const noexcept { return a_; }
@@ -87,6 +101,8 @@ class Preconditioner {
   std::size_t n_ = 0;
   const SparseMatrix* a_ = nullptr;
 };
+
+inline Preconditioner ilu0_factor(const SparseMatrix& a) { return Preconditioner::ilu0(a); }
 
 inline BlockVector precond_apply(const Preconditioner& m, const BlockVector& r,
                                  FlopCounter* flops = nullptr) {

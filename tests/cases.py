@@ -79,6 +79,26 @@ CASES = [
          dup_col=3),
     Case("maxiter3", POISSON2D_LOGUNI, 8, 8, 1, 2, 2, False, "uniform", 1e-30, 3, coeff_seed=41),
     Case("zero_rhs", POISSON2D_CONST, 8, 8, 1, 2, 2, False, "uniform", zero_rhs=True),
+    # preconditioned (preconditioners.hpp): the reference's own tests run ILU(0)
+    # (acceptance_test.cpp:70-99 OracleCorrectness instance; test_solver.cpp)
+    Case("acc32_ilu_p1", POISSON2D_LOGUNI, 32, 32, 1, 8, 1, False, "uniform", coeff_seed=7,
+         precond="ilu0"),
+    Case("acc32_ilu_p2", POISSON2D_LOGUNI, 32, 32, 1, 8, 2, False, "uniform", coeff_seed=7,
+         precond="ilu0"),
+    Case("acc32_ilu_p4", POISSON2D_LOGUNI, 32, 32, 1, 8, 4, False, "uniform", coeff_seed=7,
+         precond="ilu0"),
+    Case("acc32_ilu_p8", POISSON2D_LOGUNI, 32, 32, 1, 8, 8, False, "uniform", coeff_seed=7,
+         precond="ilu0"),
+    Case("acc32_ilu_g4", POISSON2D_LOGUNI, 32, 32, 1, 8, 4, True, "uniform", coeff_seed=7,
+         precond="ilu0"),
+    Case("acc32_jacobi_p4", POISSON2D_LOGUNI, 32, 32, 1, 8, 4, False, "uniform", coeff_seed=7,
+         precond="jacobi"),
+    Case("c2_16_ilu", LAPLACE3D_7PT, 16, 16, 16, 32, 8, False, "normal", precond="ilu0"),
+    Case("c2_16_jacobi", LAPLACE3D_7PT, 16, 16, 16, 32, 8, False, "normal", precond="jacobi"),
+    Case("x0_ilu_classical4", POISSON2D_LOGUNI, 8, 8, 1, 4, 4, False, "uniform", 1e-10,
+         coeff_seed=3, x0_seed=99, precond="ilu0"),
+    Case("dup_breakdown_ilu", POISSON2D_LOGUNI, 8, 8, 1, 4, 4, False, "uniform", coeff_seed=7,
+         dup_col=3, precond="ilu0"),
 ]
 
 # Full-size BASELINE configs whose reference solve takes minutes to hours on

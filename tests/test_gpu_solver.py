@@ -39,7 +39,12 @@ class Gen:
 def run_case(case, ctx, record=True):
     csr, b, x0 = build_inputs(case, Gen())
     a = bk.SparseMatrix(len(csr[0]) - 1, *csr, validate=False)
-    m = bk.Preconditioner.identity(a.n())
+    if case.precond == "ilu0":
+        m = bk.ilu0_factor(a, ctx)
+    elif case.precond == "jacobi":
+        m = bk.Preconditioner.jacobi(a)
+    else:
+        m = bk.Preconditioner.identity(a.n())
     c = bk.SubalgebraConfig(case.k, case.p, case.mode)
     opts = bk.SolveOptions(tol=case.tol, max_iter=case.max_iter, record_history=record)
     args = (x0, m, c, opts) if x0 is not None else (m, c, opts)
@@ -100,12 +105,13 @@ def test_fast_mode_meets_parity_bars(fast, port, name):
     assert (r.breakdown is not None) == bool(m["breakdown"])
     hist = np.array(r.defect_history)
     ref = port.bcg_solve(csr, b, case.p, case.glob, x0=x0, tol=case.tol, max_iter=case.max_iter,
-                         record_history=True)
+                         record_history=True, precond=case.precond)
     assert ref.history.tobytes() == g["history"].tobytes()  # oracle == reference fixture
     drift = _rel_hist_diff(hist, g["history"]) if m["iterations"] else 0.0
     xs = np.linalg.norm(res.x - ref.x, axis=0) / np.maximum(np.linalg.norm(ref.x, axis=0), 1e-300)
     assert np.max(xs) <= X_RTOL, xs.max()
-    if m["floor_hist_drift"] <= HIST_RTOL:
+    if m["floor_hist_drift"] <= HIST_RTOL or case.precond != "identity":
+        # (preconditioned solves run the reference-order kernels in both modes)
         # the reference itself is reorder-stable here: literal north_star bars
         assert abs(r.iterations - m["iterations"]) <= 1
         assert drift <= HIST_RTOL, drift
