@@ -296,9 +296,36 @@ struct bkg_solver {
 
   Ctrl* dctrl() { return reinterpret_cast<Ctrl*>(ctrl_buf.ptr); }
 
+  cudaGraphExec_t graph = nullptr;  // `chunk` fused iterations, captured once
+  IterArgs graph_args{};            // the arguments baked into `graph`
+
   ~bkg_solver() {
+    if (graph) cudaGraphExecDestroy(graph);
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_ring) cudaFreeHost(h_ring);
+  }
+
+  // Fast mode: the kernel arguments are fixed for the solver's lifetime, so
+  // one CUDA graph of `chunk` iterations replaces 3*chunk launches.
+  void launch_chunk() {
+    const IterArgs now = iter_args(true);
+    if (graph && std::memcmp(&now, &graph_args, sizeof(IterArgs)) != 0) {
+      cudaGraphExecDestroy(graph);  // a rebound matrix / buffer: re-capture
+      graph = nullptr;
+    }
+    if (!graph) {
+      graph_args = now;
+      cudaGraph_t g;
+      BKG_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const uint64_t before = ctx->launches;
+      for (int i = 0; i < chunk; ++i) launch_iteration(true);
+      ctx->launches = before;
+      BKG_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
+      BKG_CUDA_CHECK(cudaGraphInstantiate(&graph, g, 0));
+      cudaGraphDestroy(g);
+    }
+    BKG_CUDA_CHECK(cudaGraphLaunch(graph, ctx->stream));
+    ctx->launches += 3ull * chunk;
   }
 
   void init(bkg_ctx* c, const bkg_matrix* a, int kk, int pp, bool gl,
@@ -498,8 +525,12 @@ struct bkg_solver {
     sync(ctx);
     uint64_t seen = 0;
     while (!h_ctrl->done) {
-      const int c = cb ? 1 : chunk;
-      for (int i = 0; i < c; ++i) launch_iteration(record);
+      if (fast && !cb) {
+        launch_chunk();
+      } else {
+        const int c = cb ? 1 : chunk;
+        for (int i = 0; i < c; ++i) launch_iteration(record);
+      }
       d2h(ctx, reinterpret_cast<char*>(h_ctrl), reinterpret_cast<const char*>(dctrl()), sizeof(Ctrl));
       if (record) d2h(ctx, h_ring, hist.ptr, (size_t)ring * k);
       if (cb) {

@@ -327,3 +327,19 @@ def test_observer_sees_every_iterate(ctx):
     res = bk.bcg_solve(a, b, bk.Preconditioner.identity(64), bk.SubalgebraConfig(4, 2),
                        bk.SolveOptions(on_iterate=lambda i, x, r: seen.append(i)), ctx=ctx)
     assert seen == list(range(res.report.iterations + 1))
+
+
+def test_repeated_dropin_solves_rebind_matrix(fast):
+    # the drop-in call reuses its device workspace (and captured graph) across
+    # calls; a new matrix object must be picked up every time
+    b = bk.normal_block_rhs(16384, 8, 7)
+    first = None
+    for seed in (0, 1, 0):
+        a = bk.poisson2d(bk.PoissonSpec.heterogeneous(128, 128, 5, contrast=0.5 + seed))
+        res = bk.bcg_solve(a, b, bk.Preconditioner.identity(a.n()),
+                           bk.SubalgebraConfig.classical(8), bk.SolveOptions(max_iter=300),
+                           ctx=fast)
+        a.release_device()
+        if first is None:
+            first = res.x.copy()
+    assert res.x.tobytes() == first.tobytes()
