@@ -309,9 +309,13 @@ def run_ours(args):
     opts = bk.SolveOptions(tol=tol, max_iter=max_iter)
 
     def e2e_step():
+        t0 = time.perf_counter()
         am = bk.SparseMatrix(n, pin_off, pin_col, pin_val, validate=False)
         res = bk.bcg_solve(am, pin_b, m, cfg, opts, ctx=ctx, out=pin_x)
         am.release_device()
+        if os.environ.get("BKG_BENCH_DEBUG"):
+            print(f"e2e step {1e3 * (time.perf_counter() - t0):.1f} ms host, loop "
+                  f"{1e3 * res.report.loop_seconds:.1f} ms", file=sys.stderr)
         return res.report.iterations
 
     e2e_step()  # warm-up (allocator, module load)

@@ -267,6 +267,19 @@ __global__ void k_u64_to_i32(int64_t count, const uint64_t* __restrict__ src,
     dst[i] = (int32_t)src[i];
 }
 
+template <class T>
+void take_spare(DevBuf<T>& spare, DevBuf<T>& dst, size_t count) {
+  if (spare.count >= count && spare.count <= 2 * count + 1024)
+    dst = std::move(spare);
+  else
+    dst.alloc(count);
+}
+
+template <class T>
+void keep_spare(DevBuf<T>& spare, DevBuf<T>& src) {
+  if (src.count > spare.count) spare = std::move(src);
+}
+
 }  // namespace bkg
 
 using namespace bkg;
@@ -706,9 +719,9 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
     m->n = n;
     m->nnz = nnz;
     try {
-      m->rowptr.alloc(n + 1);
-      m->cols.alloc(std::max<uint64_t>(nnz, 1));
-      m->vals.alloc(std::max<uint64_t>(nnz, 1));
+      take_spare(ctx->spare_rowptr, m->rowptr, n + 1);
+      take_spare(ctx->spare_cols, m->cols, std::max<uint64_t>(nnz, 1));
+      take_spare(ctx->spare_vals, m->vals, std::max<uint64_t>(nnz, 1));
       h2d(ctx, reinterpret_cast<uint64_t*>(m->rowptr.ptr), off, n + 1);
       h2d(ctx, m->vals.ptr, vals, nnz);
       ctx->upload_tmp.ensure(std::max<uint64_t>(nnz, 1) * sizeof(uint64_t) + 64);
@@ -740,6 +753,9 @@ int bkg_matrix_destroy(bkg_matrix* m) {
   return guard([&] {
     if (!m) return;
     cudaSetDevice(m->ctx->device);
+    keep_spare(m->ctx->spare_rowptr, m->rowptr);
+    keep_spare(m->ctx->spare_cols, m->cols);
+    keep_spare(m->ctx->spare_vals, m->vals);
     delete m;
   });
 }

@@ -124,6 +124,11 @@ struct bkg_ctx {
   bkg::DevBuf<double> scratch;
   bkg::DevBuf<char> ctrl;  // one bkg::Ctrl for standalone kernels
   bkg::DevBuf<char> upload_tmp;  // staging for size_t column uploads
+  // CSR buffers of the last destroyed matrix, reused by the next upload
+  // (stream-ordered; saves a synchronising cudaFree + cudaMalloc per call)
+  bkg::DevBuf<int64_t> spare_rowptr;
+  bkg::DevBuf<int32_t> spare_cols;
+  bkg::DevBuf<double> spare_vals;
   // device workspace of the last bkg_solve call (reused when shapes match)
   void* solver_cache = nullptr;
   void (*solver_cache_free)(void*) = nullptr;

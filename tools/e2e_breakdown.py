@@ -13,7 +13,7 @@ import bench  # noqa: E402
 import paper_1912_11930_b200 as bk  # noqa: E402
 from paper_1912_11930_b200 import _native as N  # noqa: E402
 
-cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cfg_name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c2"
 kind, nx, ny, nz, k, p, mode, rhs, tol, max_iter, desc = bench.CONFIGS[cfg_name]
 a, b = bench.make_inputs(cfg_name, bk)
 n, nnz = a.n(), a.nnz()
@@ -26,7 +26,13 @@ px = pin((n, k), torch.float64)
 ctx = bk.Context(0, "fast")
 cfg = bk.SubalgebraConfig(k, p, mode)
 m = bk.Preconditioner.identity(n)
-for it in range(3):
+if "--after-resident" in sys.argv:  # the bench's order: resident runs first
+    s = bk.DeviceSolver(a, cfg, ctx)
+    s.set_rhs(b)
+    for _ in range(8):
+        s.run(tol, max_iter)
+    s.close()
+for it in range(4):
     t0 = time.perf_counter()
     am = bk.SparseMatrix(n, po, pc, pv, validate=False)
     h = am.device(ctx)
