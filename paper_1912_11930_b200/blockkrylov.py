@@ -10,6 +10,7 @@ step runs on the GPU through ``libbkgpu.so``; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 from dataclasses import dataclass, field
@@ -85,10 +86,14 @@ def _up(a: np.ndarray):
 class Context:
     """One device + stream + numerics mode (bkg_ctx)."""
 
+    _uids = itertools.count(1)
+
     def __init__(self, device: int = 0, numerics: str = "fast"):
         h = C.c_void_p()
         _check(N.lib().bkg_ctx_create(device, C.byref(h)))
         self.handle = h
+        # cache key for device matrices: handles can be reused after close()
+        self.uid = next(Context._uids)
         self.device = device
         self.set_numerics(numerics)
 
@@ -328,7 +333,7 @@ class SparseMatrix:
     def device(self, ctx: Optional[Context] = None):
         """Device-resident copy on ctx (uploaded once, cached)."""
         ctx = ctx or default_context()
-        key = ctx.handle.value
+        key = ctx.uid
         h = self._dev.get(key)
         if h is None:
             h = C.c_void_p()

@@ -280,9 +280,21 @@ void keep_spare(DevBuf<T>& spare, DevBuf<T>& src) {
   if (src.count > spare.count) spare = std::move(src);
 }
 
+// A device matrix is bound to the ctx that uploaded it.
+void check_owner(const bkg_ctx* ctx, const bkg_matrix* a) {
+  BKG_REQUIRE(ctx && a && a->ctx == ctx, BKG_CONFIG,
+              "matrix was uploaded on another (or a destroyed) context");
+}
+
 }  // namespace bkg
 
 using namespace bkg;
+
+// Preconditioners the fused fast loop runs (identity; Jacobi is a row scale
+// folded into K2/K3).  ILU(0) uses the unfused reference-order sequence.
+static bool fused_precond(int precond) {
+  return precond == BKG_PRECOND_IDENTITY || precond == BKG_PRECOND_JACOBI;
+}
 
 // =========================================================== solver =====
 struct bkg_solver {
@@ -295,6 +307,8 @@ struct bkg_solver {
   bool fast = false;
   FastTable ft;
   int g1 = 1, g2 = 1, g3 = 1;
+  const void* k2fn = nullptr;  // ft.k2 / ft.k2_jac (Jacobi folded into the loop)
+  const void* k3fn = nullptr;
   int ring = 66, chunk = 32;
   DevBuf<double> B, X, R, Q, Pb, Zb, coef, limits, hist, norms, partials, gpart;
   DevBuf<char> ctrl_buf;
@@ -354,7 +368,7 @@ struct bkg_solver {
     cs = nblk * p * p;
     // the fused fast loop is M = I; preconditioned solves run the unfused
     // (reference-order) kernel sequence with Z = M^-1 R on device
-    fast = use_fast(c, k, p, global, &ft) && precond == BKG_PRECOND_IDENTITY;
+    fast = use_fast(c, k, p, global, &ft) && fused_precond(precond);
     const size_t nk = (size_t)n * k;
     B.alloc(nk);
     X.alloc(nk);
@@ -375,8 +389,11 @@ struct bkg_solver {
     if (fast) {
       g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc_k1);
       const int rpc23 = ft.mma ? ft.rpc_mma : ft.rpc;
-      g2 = occupancy_grid(c, ft.k2, ft.smem_iter, n, rpc23);
-      g3 = occupancy_grid(c, ft.k3, ft.smem_iter, n, rpc23);
+      const bool jac = precond == BKG_PRECOND_JACOBI;
+      k2fn = jac ? ft.k2_jac : ft.k2;
+      k3fn = jac ? ft.k3_jac : ft.k3;
+      g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, rpc23);
+      g3 = occupancy_grid(c, k3fn, ft.smem_iter, n, rpc23);
       const int gmax = std::max(std::max(g1, g2), g3);
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
@@ -401,6 +418,7 @@ struct bkg_solver {
     a.hist_ring = ring;
     a.group = 16;
     a.ctrl = dctrl();
+    a.zscale = precond == BKG_PRECOND_JACOBI ? A->inv_diag.ptr : nullptr;
     return a;
   }
 
@@ -413,9 +431,9 @@ struct bkg_solver {
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
       launch(ctx, ft.k1, g1, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
-      launch(ctx, ft.k2, g2, kThreads, ft.smem_iter, args);
+      launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
-      launch(ctx, ft.k3, g3, kThreads, ft.smem_iter, args);
+      launch(ctx, k3fn, g3, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
       return;
     }
@@ -674,6 +692,7 @@ int bkg_ctx_destroy(bkg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->solver_cache_free) ctx->solver_cache_free(ctx->solver_cache);
+    for (bkg_matrix* m : ctx->matrices) m->ctx = nullptr;
     ctx->scratch.release();
     ctx->ctrl.release();
     cudaStreamDestroy(ctx->stream);
@@ -745,6 +764,7 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
       delete m;
       throw;
     }
+    ctx->matrices.insert(m);
     *out = m;
   });
 }
@@ -752,10 +772,13 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
 int bkg_matrix_destroy(bkg_matrix* m) {
   return guard([&] {
     if (!m) return;
-    cudaSetDevice(m->ctx->device);
-    keep_spare(m->ctx->spare_rowptr, m->rowptr);
-    keep_spare(m->ctx->spare_cols, m->cols);
-    keep_spare(m->ctx->spare_vals, m->vals);
+    if (m->ctx) {
+      cudaSetDevice(m->ctx->device);
+      m->ctx->matrices.erase(m);
+      keep_spare(m->ctx->spare_rowptr, m->rowptr);
+      keep_spare(m->ctx->spare_cols, m->cols);
+      keep_spare(m->ctx->spare_vals, m->vals);
+    }
     delete m;
   });
 }
@@ -813,6 +836,7 @@ int bkg_baxpy(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, double
 int bkg_bop(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, const double* x, double* y,
             uint64_t* flops) {
   return guard([&] {
+    check_owner(ctx, a);
     BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
     activate(ctx);
     const uint64_t n = a->n;
@@ -874,6 +898,7 @@ int bkg_column_norms(bkg_ctx* ctx, uint64_t n, uint64_t k, const double* x, doub
 int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k,
                       const double* r, double* z, uint64_t* flops) {
   return guard([&] {
+    check_owner(ctx, a);
     BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
     activate(ctx);
     const uint64_t n = a->n;
@@ -889,6 +914,7 @@ int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k
 
 int bkg_precond_setup(bkg_ctx* ctx, bkg_matrix* a, int precond, int64_t* bad_row) {
   const int st = guard([&] {
+    check_owner(ctx, a);
     BKG_REQUIRE(precond >= BKG_PRECOND_IDENTITY && precond <= BKG_PRECOND_ILU0, BKG_CONFIG,
                 "unknown preconditioner");
     activate(ctx);
@@ -901,6 +927,7 @@ int bkg_precond_setup(bkg_ctx* ctx, bkg_matrix* a, int precond, int64_t* bad_row
 int bkg_solver_create(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
                       bkg_solver** out) {
   return guard([&] {
+    check_owner(ctx, a);
     *out = nullptr;
     check_cfg(k, p, mode);
     activate(ctx);
@@ -1025,8 +1052,9 @@ int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
     const double csr = 12.0 * (double)s->A->nnz + 8.0 * (double)(s->n + 1);
     if (s->fast) {
       out[0] = 2.0 * nk8 + csr;  // K1: read P (once, neighbours via L1/L2); write Q; CSR
-      out[1] = 3.0 * nk8;        // K2: read Q, R; write R
-      out[2] = 5.0 * nk8;        // K3: read P, X, R; write P, X
+      const double jac = s->precond == BKG_PRECOND_JACOBI ? 8.0 * (double)s->n : 0.0;
+      out[1] = 3.0 * nk8 + jac;  // K2: read Q, R; write R (+ D^-1 for Jacobi)
+      out[2] = 5.0 * nk8 + jac;  // K3: read P, X, R; write P, X (+ D^-1)
     } else {  // exact mode: model of the unfused kernel sequence
       out[0] = 2.0 * nk8 + csr + 4.0 * nk8;  // spmm + alpha/rho_prev chains
       out[1] = 8.0 * nk8;                    // 2 baxpy + copy + rho/norm chains
@@ -1040,6 +1068,7 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
               const double* b, const double* x0, const bkg_solve_options* opts, double* x_out,
               double* history, uint64_t history_cap, double* final_norms, bkg_report* rep) {
   return guard([&] {
+    check_owner(ctx, a);
     check_cfg(k, p, mode);
     BKG_REQUIRE(opts != nullptr, BKG_CONFIG, "bcg_solve: options required");
     BKG_REQUIRE(opts->tol > 0.0, BKG_CONFIG, "bcg_solve: tol must be positive");
@@ -1054,7 +1083,7 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
     if (!cached || cached->n != (int64_t)a->n || cached->k != (int)k || cached->p != (int)p ||
         cached->global != glob || cached->precond != opts->precond ||
         cached->fast != (use_fast(ctx, (int)k, (int)p, glob, nullptr) &&
-                         opts->precond == BKG_PRECOND_IDENTITY)) {
+                         fused_precond(opts->precond))) {
       if (ctx->solver_cache_free) ctx->solver_cache_free(ctx->solver_cache);
       ctx->solver_cache = nullptr;
       cached = new bkg_solver();

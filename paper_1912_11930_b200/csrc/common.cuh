@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <set>
+
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -114,6 +116,8 @@ __device__ __forceinline__ bool stopped(const Ctrl* c) {
 
 }  // namespace bkg
 
+struct bkg_matrix;
+
 struct bkg_ctx {
   int device = 0;
   int numerics = BKG_NUMERICS_FAST;
@@ -129,6 +133,9 @@ struct bkg_ctx {
   bkg::DevBuf<int64_t> spare_rowptr;
   bkg::DevBuf<int32_t> spare_cols;
   bkg::DevBuf<double> spare_vals;
+  // live matrices created on this ctx (orphaned, ctx = nullptr, when the ctx
+  // is destroyed first; their buffers stay valid until bkg_matrix_destroy)
+  std::set<bkg_matrix*> matrices;
   // device workspace of the last bkg_solve call (reused when shapes match)
   void* solver_cache = nullptr;
   void (*solver_cache_free)(void*) = nullptr;

@@ -14,6 +14,8 @@ struct FastTable {
   const void* k1 = nullptr;
   const void* k2 = nullptr;
   const void* k3 = nullptr;
+  const void* k2_jac = nullptr;  // K2 / K3 with Jacobi folded in (Z = D^-1 R)
+  const void* k3_jac = nullptr;
   const void* spmm = nullptr;
   const void* gram = nullptr;
   const void* norms = nullptr;
@@ -53,11 +55,15 @@ void fill_table(FastTable* t) {
   if constexpr (P == 8 || P == 16) {  // dense p x p contraction: FP64 DMMA
     t->k2 = (const void*)&k2_mma<K, P, G>;
     t->k3 = (const void*)&k3_mma<K, P, G>;
+    t->k2_jac = (const void*)&k2_mma<K, P, G, true>;
+    t->k3_jac = (const void*)&k3_mma<K, P, G, true>;
     t->mma = true;
     t->rpc_mma = 64 * P / K;
   } else {
     t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
     t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
+    t->k2_jac = (const void*)&k2_update_gram<K, P, CPT, G, true>;
+    t->k3_jac = (const void*)&k3_update_xp<K, P, CPT, G, true>;
   }
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;

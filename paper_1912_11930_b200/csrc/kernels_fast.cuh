@@ -183,6 +183,9 @@ struct IterArgs {
   int dist;
   double* red1;
   double* red2;
+  // Jacobi in the fused loop: Z = zscale (.) R row-wise (zscale = D^-1,
+  // preconditioners.hpp:109-129); nullptr for M = I.
+  const double* zscale;
 };
 
 // Last-CTA epilogue shared by both numerics modes: norms[k] are the column
@@ -372,10 +375,11 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k1_spmm_gram
 }
 
 // ---------------------------------------------------------------- K2 ----
-// R -= Q lambda; rho = <<R, R>> (Z = M^-1 R = R) and ||R_s||^2; last CTA:
+// R -= Q lambda; rho = <<Z, R>> (Z = M^-1 R: R, or D^-1 R for Jacobi) and
+// ||R_s||^2; last CTA:
 // beta = rho_prev^-1 rho, history, stop test.  X += P lambda is deferred to
 // K3, which reads P anyway (nothing reads X before K3).
-template <int K, int P, int CPT, bool GLOBAL>
+template <int K, int P, int CPT, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gram(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
@@ -397,15 +401,17 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
   const int64_t r1 = a.n;
   for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
        base += (int64_t)gridDim.x * L::RPC * U) {
-    double qv[U][CPT], rv[U][CPT];
+    double qv[U][CPT], rv[U][CPT], dz[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = base + u * L::RPC + slot;
 #pragma unroll
       for (int j = 0; j < CPT; ++j) qv[u][j] = rv[u][j] = 0.0;
+      dz[u] = 1.0;
       if (row < r1) {
         ld_nc<CPT>(qv[u], a.Q + row * K + col0);
         ld_rw<CPT>(rv[u], a.R + row * K + col0);
+        if constexpr (JAC) dz[u] = __ldg(a.zscale + row);
       }
     }
 #pragma unroll
@@ -430,10 +436,12 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
       for (int s = 0; s < L::GT; ++s) {
 #pragma unroll
         for (int jj = 0; jj < CPT; ++jj) {
-          const double rs = __shfl_sync(kFull, rv[u][jj], gbase + s);
+          // rho = <<Z, R>>: Z = D^-1 R for Jacobi, R for M = I
+          double zs = __shfl_sync(kFull, rv[u][jj], gbase + s);
+          if constexpr (JAC) zs *= dz[u];
           const int aa = s * CPT + jj;
 #pragma unroll
-          for (int j = 0; j < CPT; ++j) acc[aa * CPT + j] = fma(rs, rv[u][j], acc[aa * CPT + j]);
+          for (int j = 0; j < CPT; ++j) acc[aa * CPT + j] = fma(zs, rv[u][j], acc[aa * CPT + j]);
         }
       }
 #pragma unroll
@@ -472,9 +480,9 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
 
 // ---------------------------------------------------------------- K3 ----
 // X += P lambda (always, once K2 ran: solver.hpp:171-175 precede the beta
-// solve and the stop test); unless the solve stopped: P = R + P beta in
+// solve and the stop test); unless the solve stopped: P = Z + P beta in
 // place (solver.hpp:186-190) and rho_prev' = <<P', R>> for the next K1.
-template <int K, int P, int CPT, bool GLOBAL>
+template <int K, int P, int CPT, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
@@ -503,23 +511,26 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   const int64_t r1 = a.n;
   for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
        base += (int64_t)gridDim.x * L::RPC * U) {
-    double pv[U][CPT], xv[U][CPT], rv[U][CPT];
+    double pv[U][CPT], xv[U][CPT], rv[U][CPT], dz[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = base + u * L::RPC + slot;
 #pragma unroll
       for (int j = 0; j < CPT; ++j) pv[u][j] = xv[u][j] = rv[u][j] = 0.0;
+      dz[u] = 1.0;
       if (row < r1) {
         ld_rw<CPT>(pv[u], a.P + row * K + col0);
         ld_rw<CPT>(xv[u], a.X + row * K + col0);
         if (!fin) ld_nc<CPT>(rv[u], a.R + row * K + col0);
+        if constexpr (JAC)
+          if (!fin) dz[u] = __ldg(a.zscale + row);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      double pn[CPT];
+      double pn[CPT];  // Z = D^-1 R (Jacobi) or R
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) pn[j] = rv[u][j];
+      for (int j = 0; j < CPT; ++j) pn[j] = JAC ? rv[u][j] * dz[u] : rv[u][j];
 #pragma unroll
       for (int s = 0; s < L::GT; ++s) {
 #pragma unroll

@@ -98,7 +98,8 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms, bool
 }
 
 // ------------------------------------------------------------ K2 (DMMA) --
-// R -= Q lambda; rho = <<R, R>>; ||R_s||^2; last CTA: beta, history, stop.
+// R -= Q lambda; rho = <<Z, R>> (Z = D^-1 R for Jacobi, R for M = I);
+// ||R_s||^2; last CTA: beta, history, stop.
 // Resident CTAs per SM (register cap) for the DMMA K2/K3, measured on B200
 // (tools/kernel_sweep.py): P = 8 tiles are small enough for 4 CTAs (64 regs);
 // at P = 16, K2 peaks at 3 and K3 (two coefficient blocks) at 2.
@@ -106,7 +107,7 @@ template <int P, int KERNEL>
 constexpr int mma_minb() {
   return P == 8 ? 4 : (KERNEL == 2 ? 3 : 2);
 }
-template <int K, int P, bool GLOBAL>
+template <int K, int P, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
@@ -129,9 +130,16 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
        rb += wstride) {
     const int64_t row = rb * 8 + (lane >> 2);
     const bool ok = row < a.n;
-    double qa[L::KC], rc[L::NT][2];
+    double qa[L::KC], rc[L::NT][2], dt[2] = {1.0, 1.0};
 #pragma unroll
     for (int kc = 0; kc < L::KC; ++kc) qa[kc] = ok ? __ldg(a.Q + row * K + col_a + kc * 4) : 0.0;
+    if constexpr (JAC) {  // Jacobi scale of the T-layout rows 4c + (lane & 3)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int64_t rt = rb * 8 + 4 * c + (lane & 3);
+        dt[c] = rt < a.n ? __ldg(a.zscale + rt) : 0.0;
+      }
+    }
 #pragma unroll
     for (int nt = 0; nt < L::NT; ++nt) {
       double t[2] = {0.0, 0.0};
@@ -149,17 +157,21 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
       acc[NG + nt * 2] = fma(rc[nt][0], rc[nt][0], acc[NG + nt * 2]);
       acc[NG + nt * 2 + 1] = fma(rc[nt][1], rc[nt][1], acc[NG + nt * 2 + 1]);
     }
-    double tr[L::NT][2];
+    double tr[L::NT][2], tz[L::NT][2];
 #pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) d_to_t(rc[nt], tr[nt], lane);
+    for (int nt = 0; nt < L::NT; ++nt) {
+      d_to_t(rc[nt], tr[nt], lane);
+      tz[nt][0] = JAC ? tr[nt][0] * dt[0] : tr[nt][0];  // rho = <<Z, R>>
+      tz[nt][1] = JAC ? tr[nt][1] * dt[1] : tr[nt][1];
+    }
 #pragma unroll
     for (int at = 0; at < L::NT; ++at)
 #pragma unroll
       for (int bt = 0; bt < L::NT; ++bt) {
         double* gacc = acc + (at * L::NT + bt) * 2;
         double d[2] = {gacc[0], gacc[1]};
-        dmma(d, tr[at][0], tr[bt][0]);
-        dmma(d, tr[at][1], tr[bt][1]);
+        dmma(d, tz[at][0], tr[bt][0]);
+        dmma(d, tz[at][1], tr[bt][1]);
         gacc[0] = d[0];
         gacc[1] = d[1];
       }
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
 
 // ------------------------------------------------------------ K3 (DMMA) --
 // X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
-template <int K, int P, bool GLOBAL>
+template <int K, int P, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
@@ -238,6 +250,14 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
     if (!fin) {
 #pragma unroll
       for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tr[nt], lane);  // R, T layout
+      if constexpr (JAC) {  // P' = Z + P beta with Z = D^-1 R (Jacobi)
+        const double dz = ok ? __ldg(a.zscale + row) : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < L::NT; ++nt) {
+          pn[nt][0] *= dz;
+          pn[nt][1] *= dz;
+        }
+      }
     }
 #pragma unroll
     for (int nt = 0; nt < L::NT; ++nt)

@@ -173,3 +173,73 @@ def test_energy_error_monotone_with_ilu(ctx):
     bk.bcg_solve(a, b, bk.ilu0_factor(a, ctx), bk.SubalgebraConfig.classical(4), opts, ctx=ctx)
     e = np.array(energy)
     assert np.all(e[1:] <= e[:-1] * (1 + 1e-10) + 1e-14)
+
+
+# ------------------------------------------- Jacobi in the fused fast loop --
+def test_jacobi_flop_totals_follow_iteration_count(ctx):
+    # test_solver.cpp:358-377 with Jacobi: n*k multiplies per apply
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(8, 8, 61))
+    n, k, p, z = 64, 4, 2, a.nnz()
+    b = bk.random_block_rhs(n, k, 62)
+    res = bk.bcg_solve(a, b, bk.Preconditioner.jacobi(a), bk.SubalgebraConfig(k, p), ctx=ctx)
+    i = res.report.iterations
+    assert res.report.converged and i >= 1
+    f = res.report.flops
+    assert f.multiply_adds_bdot == 3 * i * 2 * n * p * p * (k // p)
+    assert f.multiply_adds_bop == i * 2 * k * z
+    assert f.multiply_adds_precond == (i + 1) * n * k
+
+
+@pytest.mark.parametrize("k", [4, 8, 16])
+def test_parallel_with_jacobi_matches_columnwise_pcg(ctx, k):
+    # test_solver.cpp:153-190 with M = D: p = 1 block CG == scalar PCG per column
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(16, 16, 7))
+    n, iters = 256, 15
+    b = bk.random_block_rhs(n, k, 8)
+    m = bk.Preconditioner.jacobi(a)
+    blk = _iterates(a, b, m, bk.SubalgebraConfig.parallel(k), iters, ctx)
+    A = dense(a)
+    dinv = 1.0 / np.diag(A)
+    for c in range(k):
+        x = np.zeros(n)
+        r = b[:, c].copy()
+        p = dinv * r
+        its = [x.copy()]
+        for _ in range(iters):
+            qv = A @ p
+            alpha, rho_prev = p @ qv, p @ r
+            lam = rho_prev / alpha
+            x = x + lam * p
+            r = r - lam * qv
+            z = dinv * r
+            p = z + ((z @ r) / rho_prev) * p
+            its.append(x.copy())
+        for i in range(iters + 1):
+            np.testing.assert_allclose(blk[i][:, c], its[i], atol=1e-12 * (1 + np.abs(its[i]).max()))
+
+
+@pytest.mark.parametrize("k,p,mode", [(16, 8, "hybrid"), (32, 16, "hybrid"), (8, 4, "global"),
+                                      (16, 4, "hybrid"), (8, 1, "hybrid")])
+def test_fused_jacobi_matches_reference_order(k, p, mode):
+    # 3D 7-point with log-uniform coefficients (reorder-stable: floor ~1e-12):
+    # the fused loop (K2/K3 scale by D^-1) against the exact-order kernels,
+    # which are bit-identical to the reference (c2_16_jacobi fixture).
+    a = bk.stencil(3, 14, 13, 12, seed=5)
+    b = bk.normal_block_rhs(a.n(), k, 7)
+    m = bk.Preconditioner.jacobi(a)
+    cfg = bk.SubalgebraConfig(k, p, mode)
+    opts = bk.SolveOptions(tol=1e-10, record_history=True)
+    out = {}
+    for mode_name in ("exact", "fast"):
+        c = bk.Context(0, mode_name)
+        out[mode_name] = bk.bcg_solve(a, b, m, cfg, opts, ctx=c)
+        c.close()
+    e, f = out["exact"], out["fast"]
+    assert e.report.converged and f.report.converged
+    assert abs(e.report.iterations - f.report.iterations) <= 1
+    he, hf = np.array(e.report.defect_history), np.array(f.report.defect_history)
+    rows = min(len(he), len(hf))
+    assert np.max(np.abs(hf[:rows] - he[:rows]) / np.abs(he[:rows])) <= 1e-9
+    xs = np.linalg.norm(f.x - e.x, axis=0) / np.linalg.norm(e.x, axis=0)
+    assert xs.max() <= 1e-8
+    assert f.report.flops.multiply_adds_precond == e.report.flops.multiply_adds_precond
