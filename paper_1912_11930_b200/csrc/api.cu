@@ -388,12 +388,11 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
       g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc_k1);
-      const int rpc23 = ft.mma ? ft.rpc_mma : ft.rpc;
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
       k3fn = jac ? ft.k3_jac : ft.k3;
-      g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, rpc23);
-      g3 = occupancy_grid(c, k3fn, ft.smem_iter, n, rpc23);
+      g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, ft.rpc_k2);
+      g3 = occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3);
       const int gmax = std::max(std::max(g1, g2), g3);
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);

@@ -28,8 +28,8 @@ struct FastTable {
   int e_iter = 0;      // partial entries per CTA (max of k1, k2)
   int e_gram = 0;
   int e_norms = 0;
-  bool mma = false;  // K2/K3 are the DMMA kernels
-  int rpc_mma = 1;    // their rows per CTA pass (8 rows per warp, Q warps per row block)
+  int rpc_k2 = 1;     // rows per CTA pass of K2 / K3 (grid sizing)
+  int rpc_k3 = 1;
   int rpc_k1 = 1;     // rows per CTA pass of K1
 };
 
@@ -52,18 +52,32 @@ void fill_table(FastTable* t) {
     t->k1 = (const void*)&k1_spmm_gram<K, P, CPT, G>;
     t->rpc_k1 = Layout<K, P, CPT>::RPC;
   }
-  if constexpr (P == 8 || P == 16) {  // dense p x p contraction: FP64 DMMA
+  // K2 / K3: p x p contraction on FP64 DMMA (P < 8: block-diagonal tiles) or
+  // the scalar kernels, per kernel as measured on B200 (tools/kernel_sweep.py,
+  // DESIGN.md §5): DMMA always for P >= 8; for P < 8 the DMMA K3 wins for
+  // K <= 32 (up to 1.55x) and the DMMA K2 only at P = 4; at K = 64 the scalar
+  // kernels' full-line row accesses win.
+  constexpr bool MMA_OK = K % 8 == 0 && P <= 16;
+  constexpr bool K2_MMA = MMA_OK && (P >= 8 || (P == 4 && K <= 32));
+  constexpr bool K3_MMA = MMA_OK && (P >= 8 || K <= 32);
+  constexpr int RPC_MMA = 64 * (P < 8 ? 8 : P) / K;  // 8 rows x (8 warps / tile groups per row)
+  if constexpr (K2_MMA) {
     t->k2 = (const void*)&k2_mma<K, P, G>;
-    t->k3 = (const void*)&k3_mma<K, P, G>;
     t->k2_jac = (const void*)&k2_mma<K, P, G, true>;
-    t->k3_jac = (const void*)&k3_mma<K, P, G, true>;
-    t->mma = true;
-    t->rpc_mma = 64 * P / K;
+    t->rpc_k2 = RPC_MMA;
   } else {
     t->k2 = (const void*)&k2_update_gram<K, P, CPT, G>;
-    t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
     t->k2_jac = (const void*)&k2_update_gram<K, P, CPT, G, true>;
+    t->rpc_k2 = Layout<K, P, CPT>::RPC;
+  }
+  if constexpr (K3_MMA) {
+    t->k3 = (const void*)&k3_mma<K, P, G>;
+    t->k3_jac = (const void*)&k3_mma<K, P, G, true>;
+    t->rpc_k3 = RPC_MMA;
+  } else {
+    t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
     t->k3_jac = (const void*)&k3_update_xp<K, P, CPT, G, true>;
+    t->rpc_k3 = Layout<K, P, CPT>::RPC;
   }
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;

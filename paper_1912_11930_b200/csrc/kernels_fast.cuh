@@ -224,7 +224,9 @@ struct FastSmem {
   static constexpr int CS = NB * P * P;
   // largest TPR * NACC over the scalar K1..K3 and the DMMA K2/K3 (P >= 8)
   static constexpr int RED_SCALAR = K * P + K;
-  static constexpr int RED_MMA = (P >= 8) ? 32 * (K / P) * (2 * (P / 8) * (P / 8) + 2 * (P / 8)) : 0;
+  static constexpr int PE = P < 8 ? 8 : P;  // DMMA group width (kernels_mma.cuh MmaLayout)
+  static constexpr int RED_MMA =
+      (K % 8 == 0) ? 32 * (K / PE) * (2 * (PE / 8) * (PE / 8) + 2 * (PE / 8)) : 0;
   // K1 warp-tile kernel (kernels_mma.cuh k1_tile): 32*QW positions x 2*NPAIR
   static constexpr int W1 = K >= 16 ? 16 : 8;
   static constexpr int RED_K1 =

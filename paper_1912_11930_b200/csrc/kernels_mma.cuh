@@ -42,28 +42,45 @@ __device__ __forceinline__ void d_to_t(const double (&d)[2], double (&t)[2], int
   }
 }
 
+// A warp works on PE = max(P, 8) columns of a row block ("tile group"): one
+// p-group for P >= 8, or 8/P whole p-groups for P < 8, whose coefficient
+// blocks then form a block-diagonal 8 x 8 B operand (the zero blocks cost
+// DMMA issue slots only, which are idle in these HBM-bound kernels).
 template <int K, int P, bool GLOBAL>
 struct MmaLayout {
-  static constexpr int Q = K / P;     // p-groups per row
-  static constexpr int NT = P / 8;    // 8-column output tiles per group
-  static constexpr int KC = P / 4;    // 4-column k-chunks per group
+  static constexpr int PE = P < 8 ? 8 : P;
+  static constexpr int Q = K / PE;    // tile groups per row
+  static constexpr int NT = PE / 8;   // 8-column output tiles per tile group
+  static constexpr int KC = PE / 4;   // 4-column k-chunks per tile group
   static constexpr int TPR = 32 * Q;  // grid_reduce positions: (warp % Q, lane)
-  static constexpr int NB = GLOBAL ? 1 : Q;
+  static constexpr int NB = GLOBAL ? 1 : K / P;  // coefficient blocks
   static constexpr int CS = NB * P * P;
-  static_assert(P == 8 || P == 16, "DMMA path is for P in {8, 16}");
+  static_assert(K % 8 == 0 && P <= 16, "DMMA path: K a multiple of 8, P <= 16");
   static_assert(8 % Q == 0 || Q > 8, "warps per CTA must cover whole groups");
 };
 
-// B fragments of a p x p coefficient block c (row-major, c[b][a]):
-// frag[kc][nt] = sign * c[kc*4 + (lane&3)][nt*8 + (lane>>2)].
-template <int P>
-__device__ __forceinline__ void load_bfrag(const double* c, double sign,
-                                           double (&f)[P / 4][P / 8], int lane) {
+// B fragments of tile group g: frag[kc][nt] = sign * B[kc*4 + (lane&3)][nt*8 +
+// (lane>>2)] where B is the group's coefficient block (row-major c[b][a],
+// kernels.hpp:94-125 right-multiplication) for P >= 8, or the block-diagonal
+// embedding of its 8/P blocks for P < 8 (global: block 0 everywhere).
+template <int K, int P, bool GLOBAL>
+__device__ __forceinline__ void load_bfrag(const double* coef, int g, double sign,
+                                           double (&f)[MmaLayout<K, P, GLOBAL>::KC]
+                                                      [MmaLayout<K, P, GLOBAL>::NT],
+                                           int lane) {
+  using L = MmaLayout<K, P, GLOBAL>;
 #pragma unroll
-  for (int kc = 0; kc < P / 4; ++kc)
+  for (int kc = 0; kc < L::KC; ++kc)
 #pragma unroll
-    for (int nt = 0; nt < P / 8; ++nt)
-      f[kc][nt] = sign * c[(kc * 4 + (lane & 3)) * P + nt * 8 + (lane >> 2)];
+    for (int nt = 0; nt < L::NT; ++nt) {
+      const int b = kc * 4 + (lane & 3), a = nt * 8 + (lane >> 2);
+      if constexpr (P >= 8) {
+        f[kc][nt] = sign * coef[(GLOBAL ? 0 : g) * P * P + b * P + a];
+      } else {
+        const int blk = GLOBAL ? 0 : (g * 8 + b) / P;
+        f[kc][nt] = (b / P == a / P) ? sign * coef[blk * P * P + (b % P) * P + a % P] : 0.0;
+      }
+    }
 }
 
 // Grid totals of a Gram accumulator in D layout (per (group, lane) position
@@ -73,12 +90,16 @@ __device__ void gather_gram_mma(const double* red, int off, double* blocks) {
   using L = MmaLayout<K, P, GLOBAL>;
   for (int idx = threadIdx.x; idx < L::NB * P * P; idx += kThreads) {
     const int blk = idx / (P * P), a = (idx / P) % P, b = idx % P;
-    const int at = a >> 3, bt = b >> 3;
-    const int lane = ((a & 7) << 2) | ((b & 7) >> 1), i = b & 1;
-    const int e = off + (at * L::NT + bt) * 2 + i;
     double s = 0.0;
-    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? L::Q : blk + 1;
-    for (int g = g0; g < g1; ++g) s += red[(g * 32 + lane) * NACC + e];
+    // p-groups summed into this block (global: all of them, in order)
+    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? K / P : blk + 1;
+    for (int g = g0; g < g1; ++g) {
+      const int tg = g * P / L::PE, o = g * P % L::PE;  // tile group, column offset
+      const int ca = o + a, cb = o + b;
+      const int lane = ((ca & 7) << 2) | ((cb & 7) >> 1), i = cb & 1;
+      const int e = off + ((ca >> 3) * L::NT + (cb >> 3)) * 2 + i;
+      s += red[(tg * 32 + lane) * NACC + e];
+    }
     blocks[idx] = s;
   }
 }
@@ -90,7 +111,7 @@ template <int K, int P, bool GLOBAL, int NACC>
 __device__ void gather_norms_mma(const double* red, int off, double* norms, bool squares) {
   using L = MmaLayout<K, P, GLOBAL>;
   for (int c = threadIdx.x; c < K; c += kThreads) {
-    const int g = c / P, cc = c % P, nt = cc >> 3, i = cc & 1, l4 = (cc & 7) >> 1;
+    const int g = c / L::PE, cc = c % L::PE, nt = cc >> 3, i = cc & 1, l4 = (cc & 7) >> 1;
     double s = 0.0;
     for (int r = 0; r < 8; ++r) s += red[(g * 32 + (r << 2) + l4) * NACC + off + nt * 2 + i];
     norms[c] = squares ? s : sqrt(s);
@@ -105,7 +126,7 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms, bool
 // at P = 16, K2 peaks at 3 and K3 (two coefficient blocks) at 2.
 template <int P, int KERNEL>
 constexpr int mma_minb() {
-  return P == 8 ? 4 : (KERNEL == 2 ? 3 : 2);
+  return P <= 8 ? 4 : (KERNEL == 2 ? 3 : 2);
 }
 template <int K, int P, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs a) {
@@ -115,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = warp % L::Q;
   double nlam[L::KC][L::NT];
-  load_bfrag<P>(a.coef + (GLOBAL ? 0 : g) * P * P, -1.0, nlam, lane);
+  load_bfrag<K, P, GLOBAL>(a.coef, g, -1.0, nlam, lane);
   constexpr int NG = L::NT * L::NT * 2;  // Gram accumulators
   constexpr int NACC = NG + L::NT * 2;   // + column sums of squares
   static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
@@ -124,8 +145,8 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
   const int64_t nrb = (a.n + 7) >> 3;
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
-  const int col_a = g * P + (lane & 3);            // A-fragment column base
-  const int col_c = g * P + 2 * (lane & 3);        // C-fragment column base
+  const int col_a = g * L::PE + (lane & 3);            // A-fragment column base
+  const int col_c = g * L::PE + 2 * (lane & 3);        // C-fragment column base
   for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
        rb += wstride) {
     const int64_t row = rb * 8 + (lane >> 2);
@@ -214,10 +235,9 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   const bool fin = stopped(a.ctrl);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = warp % L::Q;
-  const double* cb = a.coef + (GLOBAL ? 0 : g) * P * P;
   double lam[L::KC][L::NT], bet[L::KC][L::NT];
-  load_bfrag<P>(cb, 1.0, lam, lane);
-  load_bfrag<P>(cb + 2 * S::CS, 1.0, bet, lane);
+  load_bfrag<K, P, GLOBAL>(a.coef, g, 1.0, lam, lane);
+  load_bfrag<K, P, GLOBAL>(a.coef + 2 * S::CS, g, 1.0, bet, lane);
   constexpr int NACC = L::NT * L::NT * 2;
   static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
@@ -225,8 +245,8 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   for (int e = 0; e < NACC; ++e) acc[e] = 0.0;
   const int64_t nrb = (a.n + 7) >> 3;
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
-  const int col_a = g * P + (lane & 3);
-  const int col_c = g * P + 2 * (lane & 3);
+  const int col_a = g * L::PE + (lane & 3);
+  const int col_c = g * L::PE + 2 * (lane & 3);
   for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
        rb += wstride) {
     const int64_t row = rb * 8 + (lane >> 2);

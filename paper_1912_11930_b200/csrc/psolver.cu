@@ -242,9 +242,8 @@ struct bkg_psolver {
       pt.ctrl_buf.alloc(sizeof(Ctrl));
       BKG_CUDA_CHECK(cudaMemsetAsync(pt.ctrl_buf.ptr, 0, sizeof(Ctrl), ctx->stream));
       pt.g1 = occupancy_grid(ctx, ft.k1, ft.smem_iter, pt.nloc, ft.rpc_k1);
-      const int rpc23 = ft.mma ? ft.rpc_mma : ft.rpc;
-      pt.g2 = occupancy_grid(ctx, ft.k2, ft.smem_iter, pt.nloc, rpc23);
-      pt.g3 = occupancy_grid(ctx, ft.k3, ft.smem_iter, pt.nloc, rpc23);
+      pt.g2 = occupancy_grid(ctx, ft.k2, ft.smem_iter, pt.nloc, ft.rpc_k2);
+      pt.g3 = occupancy_grid(ctx, ft.k3, ft.smem_iter, pt.nloc, ft.rpc_k3);
       const int gmax = std::max(std::max(pt.g1, pt.g2), pt.g3);
       pt.partials.alloc((size_t)gmax * ft.e_iter);
       pt.gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);

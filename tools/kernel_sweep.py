@@ -2,7 +2,7 @@
 """Per-kernel device times of the fused Block-CG iteration for each library
 variant under paper_1912_11930_b200/_build/variants/ (or the default build).
 
-    python tools/kernel_sweep.py [--configs c2,c4c] [--variants a,b] [--iters 20]
+    python tools/kernel_sweep.py [--configs c2,c4c,3:96:96:96:32:4:hybrid] [--variants a,b]
 
 Each variant runs in its own subprocess (BKG_LIB selects the .so)."""
 import argparse
@@ -20,6 +20,10 @@ def child(cfg, iters):
     import numpy as np
     import bench
     import paper_1912_11930_b200 as bk
+    if ":" in cfg:  # ad-hoc shape "kind:nx:ny:nz:k:p:mode" (tuning only)
+        f = cfg.split(":")
+        bench.CONFIGS[cfg] = (int(f[0]), int(f[1]), int(f[2]), int(f[3]), int(f[4]), int(f[5]),
+                              f[6], "normal", 1e-8, 0, "ad-hoc")
     kind, nx, ny, nz, k, p, mode, rhs, tol, max_iter, desc = bench.CONFIGS[cfg]
     a, b = bench.make_inputs(cfg, bk)
     s = bk.DeviceSolver(a, bk.SubalgebraConfig(k, p, mode))
