@@ -126,6 +126,12 @@ typedef struct {
   int32_t precond;     /* BKG_PRECOND_*                               */
   bkg_iterate_fn on_iterate; /* nullable */
   void* user;
+  /* Per-kernel-class device seconds into bkg_report.seconds_* (KernelSeconds,
+   * solver.hpp:41-46): the loop runs launch by launch with CUDA events at the
+   * class boundaries instead of as a captured graph.  Fast mode times its
+   * fused kernels: K1 (SpMM + alpha) as bop, K2 + K3 as baxpy; their Grams
+   * are fused, so seconds_bdot stays 0.  0: not timed (all zeros).         */
+  int32_t time_kernels;
 } bkg_solve_options;
 
 /* bcg_solve (solver.hpp:106-209, X0 = 0 overload :212-216 when x0 == NULL).

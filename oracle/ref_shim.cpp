@@ -196,4 +196,80 @@ double bkref_bench_solve(int threads, size_t n, const uint64_t* rowptr, const ui
   return dt;
 }
 
+// ---- host-side modules (perf_model.hpp, theory.hpp, text formats) -------
+// out = {omega, beta, tau}; returns 0, or -1 on ConfigError.
+int bkref_characteristics(int kernel, size_t n, size_t k, size_t p, size_t z, uint64_t* out) {
+  try {
+    const KernelCharacteristics c = characteristics(static_cast<Kernel>(kernel), n, k, p, z);
+    out[0] = c.omega;
+    out[1] = c.beta;
+    out[2] = c.tau;
+    return 0;
+  } catch (const Error&) {
+    return -1;
+  }
+}
+
+// out = {t_comp, t_mem, t_reg, t}; *bound = Bound enum value.
+int bkref_predict(int kernel, size_t n, size_t k, size_t p, size_t z, double peak, double mem,
+                  double reg, double bps, double* out, int* bound) {
+  try {
+    const MachineProfile m{peak, mem, reg, bps};
+    const Prediction pr = predict(characteristics(static_cast<Kernel>(kernel), n, k, p, z), m);
+    out[0] = pr.t_comp;
+    out[1] = pr.t_mem;
+    out[2] = pr.t_reg;
+    out[3] = pr.t;
+    *bound = static_cast<int>(pr.bound);
+    return 0;
+  } catch (const Error&) {
+    return -1;
+  }
+}
+
+double bkref_rate(int global, size_t count, const double* ev, size_t p, size_t q) {
+  const Spectrum s(std::vector<double>(ev, ev + count));
+  return global ? rate_global(s, p, q) : rate_classical(s, p);
+}
+
+void bkref_spectrum_of(size_t n, const uint64_t* rowptr, const uint64_t* cols, const double* vals,
+                       double* out) {
+  const Spectrum s = spectrum_of(to_csr(n, rowptr, cols, vals));
+  std::copy(s.values().begin(), s.values().end(), out);
+}
+
+void bkref_save_matrix_market(const char* path, size_t n, const uint64_t* rowptr,
+                              const uint64_t* cols, const double* vals) {
+  save_matrix_market(path, to_csr(n, rowptr, cols, vals));
+}
+
+void bkref_save_block_vector(const char* path, size_t n, size_t k, const double* x) {
+  save_block_vector(path, to_bv(n, k, x));
+}
+
+// Reads a Matrix Market file and writes it back in the reference's canonical
+// form (the read semantics: mirroring, duplicate summation, validation).
+// Returns 0, 1 on IoError, 2 on another blockkrylov error.
+int bkref_mm_roundtrip(const char* in, const char* out) {
+  try {
+    save_matrix_market(out, load_matrix_market(in));
+    return 0;
+  } catch (const IoError&) {
+    return 1;
+  } catch (const Error&) {
+    return 2;
+  }
+}
+
+int bkref_bv_roundtrip(const char* in, const char* out) {
+  try {
+    save_block_vector(out, load_block_vector(in));
+    return 0;
+  } catch (const IoError&) {
+    return 1;
+  } catch (const Error&) {
+    return 2;
+  }
+}
+
 }  // extern "C"

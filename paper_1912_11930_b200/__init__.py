@@ -11,5 +11,7 @@ from .blockkrylov import (BlockCoefficient, BreakdownError, ConfigError, Context
                           SubalgebraConfig, baxpy, bcg_solve, bdot, bop, bsolve, column_norms,
                           default_context, set_numerics)
 from .resident import DeviceSolver  # noqa: F401
+from .textio import (IoError, load_block_vector, load_matrix_market,  # noqa: F401
+                     save_block_vector, save_matrix_market)
 
 __version__ = "0.1.0"

@@ -65,6 +65,7 @@ class SolveOptions(C.Structure):
         ("precond", C.c_int32),
         ("on_iterate", ITERATE_FN),
         ("user", C.c_void_p),
+        ("time_kernels", C.c_int32),
     ]
 
 

@@ -522,6 +522,8 @@ class SolveOptions:
     max_iter: int = 0
     record_history: bool = False
     on_iterate: Optional[Callable[[int, np.ndarray, np.ndarray], None]] = None
+    # per-kernel-class device seconds into SolveReport.seconds (bkg.h time_kernels)
+    time_kernels: bool = False
 
 
 @dataclass
@@ -605,6 +607,7 @@ def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None,
     so.max_iter = int(opts.max_iter)
     so.record_history = 1 if opts.record_history else 0
     so.precond = _PREC[m.kind()]
+    so.time_kernels = 1 if opts.time_kernels else 0
     cb_holder = None
     errors: List[BaseException] = []
     if opts.on_iterate is not None:

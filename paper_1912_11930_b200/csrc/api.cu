@@ -318,6 +318,9 @@ struct bkg_solver {
   double* Z = nullptr;
   bool have_b = false;
   int precond = BKG_PRECOND_IDENTITY;
+  bool timing = false;          // SolveOptions time_kernels
+  double class_ms[4] = {};      // bdot, baxpy, bop, precond
+  cudaEvent_t tev[9] = {};
   std::vector<double> history;  // rows x k
   uint64_t history_rows = 0;
 
@@ -328,6 +331,8 @@ struct bkg_solver {
 
   ~bkg_solver() {
     if (graph) cudaGraphExecDestroy(graph);
+    for (auto e : tev)
+      if (e) cudaEventDestroy(e);
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_ring) cudaFreeHost(h_ring);
   }
@@ -422,8 +427,15 @@ struct bkg_solver {
   }
 
   // One Block-CG iteration (solver.hpp:157-201), queued on the ctx stream.
-  void launch_iteration(bool with_hist, cudaEvent_t* ev = nullptr) {
+  // ev (optional): 4 events around K1 | K2 | K3 (fast) or the coarse phases
+  // (exact); fine = true (exact only): 9 events at the kernel-class
+  // boundaries of solver.hpp:161-187 (see timed_iteration).
+  void launch_iteration(bool with_hist, cudaEvent_t* ev = nullptr, bool fine = false) {
     Ctrl* ctrl = dctrl();
+    auto mark = [&](int coarse, int fine_i) {
+      const int i = fine ? fine_i : coarse;
+      if (ev && i >= 0) BKG_CUDA_CHECK(cudaEventRecord(ev[i], ctx->stream));
+    };
     if (fast) {
       IterArgs a = iter_args(with_hist);
       void* args[] = {&a};
@@ -438,11 +450,12 @@ struct bkg_solver {
     }
     const Ctrl* cc = ctrl;
     double* cf = coef.ptr;
-    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
+    mark(0, 0);
     dev_spmm(ctx, A, k, P, Q.ptr, cc, true);                                  // Q = A P
+    mark(-1, 1);
     dev_chain(ctx, false, n, k, p, global, P, Q.ptr, cf + 4 * cs, cc);        // alpha
     dev_chain(ctx, false, n, k, p, global, P, R.ptr, cf + cs, cc);            // rho_prev
-    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
+    mark(1, 2);
     {
       const int smem = (int)sizeof(double) * bsolve_ws_doubles(p, 256);
       allow_smem((const void*)&k_exact_lambda, smem);
@@ -450,12 +463,16 @@ struct bkg_solver {
       void* args[] = {&ctrl, &nb, &pp, &cf, &c_s};
       launch(ctx, (const void*)&k_exact_lambda, 1, 256, smem, args);
     }
+    mark(-1, 3);
     dev_baxpy(ctx, n, k, p, global, X.ptr, P, cf, cc, true);                  // X += P lambda
     dev_baxpy(ctx, n, k, p, global, R.ptr, Q.ptr, cf + 5 * cs, cc, true);     // R -= Q lambda
+    mark(-1, 4);
     precond_apply_dev(ctx, const_cast<bkg_matrix*>(A), precond, k, R.ptr, Z, cc);  // Z = M^-1 R
+    mark(-1, 5);
     dev_chain(ctx, false, n, k, p, global, Z, R.ptr, cf + 3 * cs, cc);        // rho
+    mark(-1, 6);
     dev_chain(ctx, true, n, k, 1, false, R.ptr, R.ptr, norms.ptr, cc);        // ||R_s||
-    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
+    mark(2, -1);
     {
       const int smem = (int)sizeof(double) * bsolve_ws_doubles(p, 256);
       allow_smem((const void*)&k_exact_beta, smem);
@@ -466,9 +483,35 @@ struct bkg_solver {
       void* args[] = {&ctrl, &nb, &pp, &kk, &cf, &c_s, &nm, &lm, &hs, &rg};
       launch(ctx, (const void*)&k_exact_beta, 1, 256, smem, args);
     }
+    mark(-1, 7);
     dev_baxpy(ctx, n, k, p, global, Z, P, cf + 2 * cs, cc, true);             // Z += P beta
     std::swap(P, Z);                                                           // P^{i+1}
-    if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
+    mark(3, 8);
+  }
+
+  // One iteration with device time per kernel class added to class_ms
+  // [bdot, baxpy, bop, precond] (KernelSeconds order).  Exact mode: the
+  // reference's classes (column norms and the p x p solves are untimed, as
+  // in solver.hpp); fast mode: K1 = bop, K2 + K3 = baxpy (Grams fused).
+  void timed_iteration(bool with_hist) {
+    if (!tev[0])
+      for (auto& e : tev) BKG_CUDA_CHECK(cudaEventCreate(&e));
+    launch_iteration(with_hist, tev, !fast);
+    BKG_CUDA_CHECK(cudaEventSynchronize(tev[fast ? 3 : 8]));
+    auto ms = [&](int a, int b) {
+      float t = 0.f;
+      BKG_CUDA_CHECK(cudaEventElapsedTime(&t, tev[a], tev[b]));
+      return (double)t;
+    };
+    if (fast) {
+      class_ms[2] += ms(0, 1);
+      class_ms[1] += ms(1, 3);
+    } else {
+      class_ms[2] += ms(0, 1);
+      class_ms[0] += ms(1, 2) + ms(5, 6);
+      class_ms[1] += ms(3, 4) + ms(7, 8);
+      class_ms[3] += ms(4, 5);
+    }
   }
 
   bool norms_fast() const { return fast; }
@@ -555,7 +598,9 @@ struct bkg_solver {
     sync(ctx);
     uint64_t seen = 0;
     while (!h_ctrl->done) {
-      if (fast && !cb) {
+      if (timing) {
+        for (int i = 0; i < (cb ? 1 : chunk); ++i) timed_iteration(record);
+      } else if (fast && !cb) {
         launch_chunk();
       } else {
         const int c = cb ? 1 : chunk;
@@ -630,6 +675,7 @@ struct bkg_solver {
     BKG_REQUIRE(have_b, BKG_CONFIG, "solver: right hand side not set");
     BKG_REQUIRE(tol > 0.0, BKG_CONFIG, "bcg_solve: tol must be positive");
     std::memset(rep, 0, sizeof(*rep));
+    std::fill(class_ms, class_ms + 4, 0.0);
     const uint64_t max_iter = max_iter_opt ? max_iter_opt : 10ull * (uint64_t)n;
     std::vector<double> lim;
     bool x0nz = false;
@@ -644,6 +690,10 @@ struct bkg_solver {
     }
     loop(record, cb, user, &rep->loop_seconds);
     fill_report(rep, conv0);
+    rep->seconds_bdot = 1e-3 * class_ms[0];
+    rep->seconds_baxpy = 1e-3 * class_ms[1];
+    rep->seconds_bop = 1e-3 * class_ms[2];
+    rep->seconds_precond = 1e-3 * class_ms[3];
     final_residual(final_norms);
     sync(ctx);
   }
@@ -1093,6 +1143,7 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
     bkg_solver& s = *cached;
     s.A = a;
     s.precond = opts->precond;
+    s.timing = opts->time_kernels != 0;
     h2d(ctx, s.B.ptr, b, (size_t)a->n * k);
     s.have_b = true;
     s.run(x0, opts->tol, opts->max_iter, opts->record_history != 0, opts->on_iterate, opts->user,

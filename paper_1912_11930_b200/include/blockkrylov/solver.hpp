@@ -28,6 +28,9 @@ struct SolveOptions {
   std::size_t max_iter = 0;
   bool record_history = false;
   std::function<void(std::size_t, const BlockVector&, const BlockVector&)> on_iterate;
+  /// Extension: fill SolveReport::seconds with device time per kernel class
+  /// (bkg.h time_kernels; the reference always wall-clocks its kernels).
+  bool time_kernels = false;
 };
 
 struct BreakdownInfo {
@@ -101,6 +104,7 @@ inline SolveResult bcg_solve(const SparseMatrix& a, const BlockVector& b, const 
   o.max_iter = opts.max_iter;
   o.record_history = opts.record_history ? 1 : 0;
   o.precond = static_cast<int32_t>(m.kind());
+  o.time_kernels = opts.time_kernels ? 1 : 0;
   if (opts.on_iterate) {
     o.on_iterate = &detail::ObserverBridge::call;
     o.user = &bridge;

@@ -1,0 +1,174 @@
+"""blockkrylov-cli on the GPU (blockkrylov_cli.cpp:57-168, 320-510 restated):
+`solve` CSV rows against the reference solver on the same inputs (exact
+numerics: iterations, convergence, breakdown and flop counts identical),
+batching, --time, dumps and exit codes; `verify --suite all`.  Also the
+time_kernels option of the Python API."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1912_11930_b200 as bk
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_1912_11930_b200", "_build", "blockkrylov-cli")
+COLS = ("run,nx,ny,k,p,mode,precond,tol,seed,iterations,converged,breakdown_iteration,"
+        "breakdown_block,flops_bdot,flops_baxpy,flops_bop,flops_precond,seconds_bdot,"
+        "seconds_baxpy,seconds_bop,seconds_precond").split(",")
+
+
+def cli(*args, numerics="exact"):
+    env = dict(os.environ, BKG_NUMERICS=numerics)
+    return subprocess.run([CLI, *args], capture_output=True, text=True, timeout=600, env=env)
+
+
+def rows(out):
+    lines = out.stdout.strip().split("\n")
+    assert lines[0].split(",") == COLS
+    return [dict(zip(COLS, l.split(","))) for l in lines[1:]]
+
+
+def reference_rows(ref, nx, ny, k, p, glob, precond, seed, runs, tol=1e-8, max_iter=0,
+                   rhs=None, coeff="loguniform"):
+    spec = (bk.PoissonSpec.heterogeneous(nx, ny, seed) if coeff == "loguniform"
+            else bk.PoissonSpec.constant(nx, ny))
+    a = bk.poisson2d(spec)
+    csr = (a.row_offsets(), a.col_indices(), a.values())
+    allb = rhs if rhs is not None else bk.random_block_rhs(a.n(), runs * k, seed)
+    out = []
+    for r in range(runs):
+        b = np.ascontiguousarray(allb[:, r * k:(r + 1) * k])
+        out.append(ref.bcg_solve(csr, b, p, glob, tol=tol, max_iter=max_iter, precond=precond,
+                                 record_history=False).report)
+    return out
+
+
+def check_against_reference(got, want):
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert int(g["iterations"]) == w.iterations
+        assert g["converged"] == ("true" if w.converged else "false")
+        assert (g["breakdown_iteration"] != "") == bool(w.breakdown)
+        if w.breakdown:
+            assert int(g["breakdown_iteration"]) == w.breakdown_iteration
+            assert int(g["breakdown_block"]) == w.breakdown_block
+        assert int(g["flops_bdot"]) == w.flops_bdot
+        assert int(g["flops_baxpy"]) == w.flops_baxpy
+        assert int(g["flops_bop"]) == w.flops_bop
+        assert int(g["flops_precond"]) == w.flops_precond
+
+
+@pytest.mark.parametrize("args,kw", [
+    ([], dict(nx=32, ny=32, k=8, p=8, glob=False, precond="ilu0", seed=1, runs=1)),
+    (["--nx", "20", "--ny", "24", "--k", "8", "--p", "2", "--precond", "jacobi", "--seed", "4",
+      "--repetitions", "2"], dict(nx=20, ny=24, k=8, p=2, glob=False, precond="jacobi", seed=4, runs=2)),
+    (["--nx", "16", "--ny", "16", "--k", "8", "--p", "4", "--mode", "global", "--precond",
+      "identity", "--total-rhs", "24"], dict(nx=16, ny=16, k=8, p=4, glob=True, precond="identity",
+                                              seed=1, runs=3)),
+    (["--nx", "24", "--ny", "12", "--k", "4", "--coeff", "constant", "--tol", "1e-10"],
+     dict(nx=24, ny=12, k=4, p=4, glob=False, precond="ilu0", seed=1, runs=1, tol=1e-10,
+          coeff="constant")),
+])
+def test_solve_rows_match_reference_exact(ref, args, kw):
+    out = cli("solve", *args)
+    assert out.returncode == 0, out.stderr
+    got = rows(out)
+    want = reference_rows(ref, **kw)
+    check_against_reference(got, want)
+    for i, g in enumerate(got):
+        assert int(g["run"]) == i and g["precond"] == kw["precond"]
+        assert g["mode"] == ("global" if kw["glob"] else "hybrid")
+        assert float(g["seconds_bop"]) == 0.0  # untimed without --time
+
+
+def test_solve_fast_numerics_within_bars(ref):
+    out = cli("solve", "--nx", "32", "--ny", "32", "--k", "8", "--p", "4", "--precond", "jacobi",
+              numerics="fast")
+    assert out.returncode == 0, out.stderr
+    (g,) = rows(out)
+    (w,) = reference_rows(ref, 32, 32, 8, 4, False, "jacobi", 1, 1)
+    assert g["converged"] == "true"
+    assert abs(int(g["iterations"]) - w.iterations) <= max(1, w.iterations // 20)
+
+
+def test_solve_max_iter_exit_code(ref):
+    out = cli("solve", "--nx", "16", "--ny", "16", "--max-iter", "3", "--repetitions", "2")
+    assert out.returncode == 3
+    got = rows(out)
+    assert [g["converged"] for g in got] == ["false", "false"]
+    check_against_reference(got, reference_rows(ref, 16, 16, 8, 8, False, "ilu0", 1, 2, max_iter=3))
+
+
+def test_solve_breakdown_exit_code_and_columns(ref, tmp_path):
+    # duplicated right hand sides make the classical block rank deficient
+    n = 16 * 16
+    base = bk.random_block_rhs(n, 2, 9)
+    rhs = np.hstack([base, base])
+    f = tmp_path / "dup.txt"
+    bk.save_block_vector(str(f), rhs)
+    out = cli("solve", "--nx", "16", "--ny", "16", "--k", "4", "--precond", "identity",
+              "--rhs-file", str(f))
+    assert out.returncode == 2, out.stderr
+    got = rows(out)
+    want = reference_rows(ref, 16, 16, 4, 4, False, "identity", 1, 1, rhs=rhs)
+    assert want[0].breakdown
+    check_against_reference(got, want)
+
+
+def test_solve_dumps_match_writers(ref, tmp_path):
+    mtx, rhs = tmp_path / "a.mtx", tmp_path / "b.txt"
+    out = cli("solve", "--nx", "10", "--ny", "9", "--k", "4", "--seed", "3", "--repetitions", "2",
+              "--dump-matrix", str(mtx), "--dump-rhs", str(rhs))
+    assert out.returncode == 0, out.stderr
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(10, 9, 3))
+    assert bk.load_matrix_market(str(mtx)) == a
+    b = bk.load_block_vector(str(rhs))
+    assert b.tobytes() == bk.random_block_rhs(a.n(), 8, 3).tobytes()
+    py = tmp_path / "py.mtx"
+    bk.save_matrix_market(str(py), a)
+    assert py.read_bytes() == mtx.read_bytes()
+    # the dumped right hand sides, fed back, reproduce the rows
+    again = cli("solve", "--nx", "10", "--ny", "9", "--k", "4", "--seed", "3", "--rhs-file", str(rhs))
+    assert again.returncode == 0
+    assert [r["iterations"] for r in rows(again)] == [r["iterations"] for r in rows(out)]
+
+
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_solve_time_columns(numerics):
+    out = cli("solve", "--nx", "24", "--ny", "24", "--k", "8", "--p", "4", "--precond", "jacobi",
+              "--time", "--reps", "3", numerics=numerics)
+    assert out.returncode == 0, out.stderr
+    (g,) = rows(out)
+    sec = {c: float(g[c]) for c in COLS if c.startswith("seconds_")}
+    assert sec["seconds_bop"] > 0 and sec["seconds_baxpy"] > 0
+    if numerics == "exact":
+        assert sec["seconds_bdot"] > 0 and sec["seconds_precond"] > 0
+    else:  # Grams and the Jacobi scale are fused into K1..K3
+        assert sec["seconds_bdot"] == 0.0 and sec["seconds_precond"] == 0.0
+
+
+def test_verify_all_suites_pass():
+    out = cli("verify", numerics="fast")
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = out.stdout.strip().split("\n")
+    assert len(lines) == 7 and all(l.endswith("pass") for l in lines)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_time_kernels_option(mode):
+    ctx = bk.Context(0, mode)
+    a = bk.poisson2d(bk.PoissonSpec.heterogeneous(32, 32, 2))
+    b = bk.random_block_rhs(a.n(), 8, 3)
+    cfg = bk.SubalgebraConfig(8, 4)
+    m = bk.Preconditioner.identity(a.n())
+    plain = bk.bcg_solve(a, b, m, cfg, bk.SolveOptions(), ctx=ctx)
+    timed = bk.bcg_solve(a, b, m, cfg, bk.SolveOptions(time_kernels=True), ctx=ctx)
+    assert plain.report.seconds.bop == 0.0
+    assert timed.report.seconds.bop > 0 and timed.report.seconds.baxpy > 0
+    # timing changes how the loop is launched, not what it computes
+    assert timed.report.iterations == plain.report.iterations
+    assert timed.x.tobytes() == plain.x.tobytes()
+    ctx.close()
