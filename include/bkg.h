@@ -209,6 +209,19 @@ int bkg_stencil_fill(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t s
 int bkg_random_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out);
 int bkg_normal_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out);
 
+/* Device-side generation (csrc/generate.cu).  The stencil
+ * is assembled straight into a device matrix on ctx (bit-identical to
+ * bkg_stencil_fill); bkg_matrix_download copies any device matrix back.
+ * bkg_solver_generate_rhs fills the resident B: distribution 0 =
+ * random_block_rhs (bit-identical), 1 = the N(0,1) stream (Box-Muller with
+ * CUDA libm: within a few ulp of bkg_normal_block_rhs).                     */
+int bkg_matrix_generate(bkg_ctx* ctx, int kind, uint64_t nx, uint64_t ny, uint64_t nz,
+                        uint64_t seed, double contrast, bkg_matrix** out);
+int bkg_matrix_download(const bkg_matrix* m, uint64_t* row_offsets, uint64_t* cols,
+                        double* vals);
+int bkg_solver_generate_rhs(bkg_solver* s, int distribution, uint64_t seed);
+int bkg_solver_get_rhs(bkg_solver* s, double* b_host); /* the resident B    */
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@ from .blockkrylov import (BlockCoefficient, BreakdownError, ConfigError, Context
                           DimensionError, FlopCounter, Preconditioner, SolveOptions, SparseMatrix,
                           SubalgebraConfig, baxpy, bcg_solve, bdot, bop, bsolve, column_norms,
                           default_context, set_numerics)
+from .generate import DeviceMatrix  # noqa: F401
 from .resident import DeviceSolver  # noqa: F401
 from .textio import (IoError, load_block_vector, load_matrix_market,  # noqa: F401
                      save_block_vector, save_matrix_market)

@@ -83,6 +83,9 @@ SIGNATURES = [
     ("bkg_matrix_create", C.c_int, [_vp, C.c_uint64, _u, _u, _d, C.POINTER(_vp)]),
     ("bkg_matrix_destroy", C.c_int, [_vp]),
     ("bkg_matrix_info", C.c_int, [_vp, _u, _u]),
+    ("bkg_matrix_generate", C.c_int, [_vp, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      C.c_uint64, C.c_double, C.POINTER(_vp)]),
+    ("bkg_matrix_download", C.c_int, [_vp, _u, _u, _d]),
     ("bkg_bdot", C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _d, _d, _d, _u]),
     ("bkg_baxpy", C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _d, _d, _d, _u]),
     ("bkg_bop", C.c_int, [_vp, _vp, C.c_uint64, _d, _d, _u]),
@@ -95,6 +98,8 @@ SIGNATURES = [
     ("bkg_solver_create", C.c_int, [_vp, _vp, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(_vp)]),
     ("bkg_solver_destroy", C.c_int, [_vp]),
     ("bkg_solver_set_rhs", C.c_int, [_vp, _d]),
+    ("bkg_solver_generate_rhs", C.c_int, [_vp, C.c_int, C.c_uint64]),
+    ("bkg_solver_get_rhs", C.c_int, [_vp, _d]),
     ("bkg_solver_run", C.c_int, [_vp, C.c_double, C.c_uint64, C.c_int, C.POINTER(Report)]),
     ("bkg_solver_get_x", C.c_int, [_vp, _d]),
     ("bkg_solver_history", C.c_int, [_vp, _d, C.c_uint64, _u]),

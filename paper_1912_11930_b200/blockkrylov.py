@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import weakref
 import os
 import threading
 from dataclasses import dataclass, field
@@ -94,6 +95,7 @@ class Context:
         self.handle = h
         # cache key for device matrices: handles can be reused after close()
         self.uid = next(Context._uids)
+        self._children = weakref.WeakSet()
         self.device = device
         self.set_numerics(numerics)
 
@@ -113,8 +115,15 @@ class Context:
         _check(N.lib().bkg_ctx_launch_count(self.handle, C.byref(v)))
         return v.value
 
+    def adopt(self, obj) -> None:
+        """Register a native object bound to this context (it is closed first
+        when the context closes, so nothing outlives its bkg_ctx)."""
+        self._children.add(obj)
+
     def close(self) -> None:
         if self.handle:
+            for obj in list(self._children):
+                obj.close()
             N.lib().bkg_ctx_destroy(self.handle)
             self.handle = None
 

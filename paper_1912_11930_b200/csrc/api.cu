@@ -832,6 +832,50 @@ int bkg_matrix_destroy(bkg_matrix* m) {
   });
 }
 
+int bkg_matrix_generate(bkg_ctx* ctx, int kind, uint64_t nx, uint64_t ny, uint64_t nz,
+                        uint64_t seed, double contrast, bkg_matrix** out) {
+  return guard([&] {
+    *out = nullptr;
+    BKG_REQUIRE(kind >= 0 && kind <= 4, BKG_CONFIG, "stencil: unknown kind");
+    if (kind <= 2) nz = 1;
+    BKG_REQUIRE(nx >= 2 && ny >= 2 && (kind <= 2 || nz >= 2), BKG_CONFIG,
+                "stencil: grid must be at least 2 cells per axis");
+    BKG_REQUIRE(kind != 1 || contrast >= 0.0, BKG_CONFIG, "stencil: contrast must be >= 0");
+    uint64_t n = 0, nnz = 0;
+    bkg_stencil_size(kind, nx, ny, nz, &n, &nnz);
+    BKG_REQUIRE(n < (1ull << 31), BKG_CONFIG, "sparse matrix: n must be < 2^31 on device");
+    activate(ctx);
+    auto* m = new bkg_matrix();
+    m->ctx = ctx;
+    m->n = n;
+    m->nnz = nnz;
+    try {
+      take_spare(ctx->spare_rowptr, m->rowptr, n + 1);
+      take_spare(ctx->spare_cols, m->cols, nnz);
+      take_spare(ctx->spare_vals, m->vals, nnz);
+      dev_generate_stencil(ctx, kind, (int64_t)nx, (int64_t)ny, (int64_t)nz, seed, contrast, m);
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    ctx->matrices.insert(m);
+    *out = m;
+  });
+}
+
+int bkg_matrix_download(const bkg_matrix* m, uint64_t* off, uint64_t* cols, double* vals) {
+  return guard([&] {
+    BKG_REQUIRE(m->ctx, BKG_CONFIG, "matrix: its context was destroyed");
+    activate(m->ctx);
+    std::vector<int32_t> c32(m->nnz);
+    d2h(m->ctx, reinterpret_cast<int64_t*>(off), m->rowptr.ptr, m->n + 1);
+    d2h(m->ctx, c32.data(), m->cols.ptr, m->nnz);
+    d2h(m->ctx, vals, m->vals.ptr, m->nnz);
+    sync(m->ctx);
+    for (uint64_t i = 0; i < m->nnz; ++i) cols[i] = (uint64_t)c32[i];
+  });
+}
+
 int bkg_matrix_info(const bkg_matrix* m, uint64_t* n, uint64_t* nnz) {
   return guard([&] {
     *n = m->n;
@@ -1008,6 +1052,16 @@ int bkg_solver_set_rhs(bkg_solver* s, const double* b) {
   });
 }
 
+int bkg_solver_generate_rhs(bkg_solver* s, int distribution, uint64_t seed) {
+  return guard([&] {
+    BKG_REQUIRE(distribution == 0 || distribution == 1, BKG_CONFIG,
+                "rhs: distribution must be 0 (uniform) or 1 (normal)");
+    activate(s->ctx);
+    dev_generate_rhs(s->ctx, distribution, s->n, s->k, seed, s->B.ptr);
+    s->have_b = true;
+  });
+}
+
 int bkg_solver_run(bkg_solver* s, double tol, uint64_t max_iter, int record_history,
                    bkg_report* rep) {
   return guard([&] {
@@ -1020,6 +1074,15 @@ int bkg_solver_get_x(bkg_solver* s, double* x) {
   return guard([&] {
     activate(s->ctx);
     d2h(s->ctx, x, s->X.ptr, (size_t)s->n * s->k);
+    sync(s->ctx);
+  });
+}
+
+int bkg_solver_get_rhs(bkg_solver* s, double* b) {
+  return guard([&] {
+    BKG_REQUIRE(s->have_b, BKG_CONFIG, "solver: right hand side not set");
+    activate(s->ctx);
+    d2h(s->ctx, b, s->B.ptr, (size_t)s->n * s->k);
     sync(s->ctx);
   });
 }

@@ -15,6 +15,10 @@ void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void**
 void allow_smem(const void* fn, int bytes);
 int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
+// generate.cu: device-side problem generation
+void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst);
+void dev_generate_stencil(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
+                          uint64_t seed, double contrast, bkg_matrix* m);
 void check_cfg(uint64_t k, uint64_t p, int mode);
 void dev_gram(bkg_ctx* c, int64_t n, int k, int p, bool global, const double* x, const double* y,
               double* out, bool force_exact);

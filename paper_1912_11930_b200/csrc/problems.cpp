@@ -5,45 +5,64 @@
 // exp(N(0,1)) diffusion field and the 3D 7/27-point stencils are the frozen
 // synthetic inputs defined in DESIGN.md §Inputs.  Compiled with
 // -ffp-contract=off so libm-based values match the oracle's.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "bkg.h"
+#include "rng.h"
 
 namespace {
 
-// Xorshift64Star (problems.hpp:19-46).
-struct Rng {
-  uint64_t s;
-  explicit Rng(uint64_t seed) {
-    uint64_t z = seed + 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    s = z ^ (z >> 31);
-    if (s == 0) s = 0x9E3779B97F4A7C15ull;
-  }
-  uint64_t next() {
-    s ^= s >> 12;
-    s ^= s << 25;
-    s ^= s >> 27;
-    return s * 0x2545F4914F6CDD1Dull;
-  }
-  double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
-  double symmetric() { return 2.0 * unit() - 1.0; }
-};
+using namespace bkg;
 
-// Box-Muller pairs over Xorshift64Star, both outputs used, storage order.
-void normal_fill(Rng& g, uint64_t count, double* out) {
-  for (uint64_t i = 0; i < count; i += 2) {
-    const double u1 = g.unit();
-    const double u2 = g.unit();
-    const double rad = std::sqrt(-2.0 * std::log(1.0 - u1));
-    const double th = 6.283185307179586 * u2;
-    out[i] = rad * std::cos(th);
-    if (i + 1 < count) out[i + 1] = rad * std::sin(th);
+// Stream position -> state, shared by all generator threads.
+const uint64_t* jump_table() {
+  static const std::vector<uint64_t> t = [] {
+    std::vector<uint64_t> v(64 * 64);
+    rng::jump_table(v.data());
+    return v;
+  }();
+  return t.data();
+}
+
+// Runs body(begin, end, state_at_begin_draw) over [0, units) in parallel
+// chunks; `draws` draws per unit.  Chunks start from the jumped state, so the
+// result is the serial stream's bit for bit.
+template <class F>
+void parallel_stream(uint64_t seed, uint64_t units, uint64_t draws, F body) {
+  const uint64_t s0 = rng::seed_state(seed);
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const uint64_t per = std::max<uint64_t>(1u << 18, (units + hw - 1) / hw);
+  std::vector<std::thread> pool;
+  for (uint64_t b = 0; b < units; b += per) {
+    const uint64_t e = std::min(units, b + per);
+    const uint64_t s = rng::jump(jump_table(), s0, b * draws);
+    if (e == units && pool.empty()) {  // one chunk: no thread
+      body(b, e, s);
+      return;
+    }
+    pool.emplace_back([=] { body(b, e, s); });
   }
+  for (auto& t : pool) t.join();
+}
+
+// Box-Muller pairs over Xorshift64Star, both outputs used, storage order:
+// pair j consumes draws 2j, 2j+1 and writes values 2j, 2j+1.
+void normal_fill(uint64_t seed, uint64_t count, double* out) {
+  parallel_stream(seed, (count + 1) / 2, 2, [=](uint64_t b, uint64_t e, uint64_t s) {
+    for (uint64_t j = b; j < e; ++j) {
+      const double u1 = rng::unit(s);
+      const double u2 = rng::unit(s);
+      const double rad = std::sqrt(-2.0 * std::log(1.0 - u1));
+      const double th = 6.283185307179586 * u2;
+      out[2 * j] = rad * std::cos(th);
+      if (2 * j + 1 < count) out[2 * j + 1] = rad * std::sin(th);
+    }
+  });
 }
 
 inline double harmonic(double a, double b) { return 2.0 * a * b / (a + b); }
@@ -102,6 +121,22 @@ void assemble3d(uint64_t nx, uint64_t ny, uint64_t nz, bool full27, uint64_t* of
 
 }  // namespace
 
+namespace bkg {
+// Cell coefficients of the 2D generators: kind 1 = 10^(contrast * U(-1,1))
+// (problems.hpp:90-99), kind 2 = exp(N(0,1)).  Host libm,
+// so the device assembler (generate.cu) uses these same bits.
+void coefficient_field(int kind, uint64_t seed, double contrast, uint64_t n, double* coeff) {
+  if (kind == 1) {
+    parallel_stream(seed, n, 1, [=](uint64_t b, uint64_t e, uint64_t s) {
+      for (uint64_t i = b; i < e; ++i) coeff[i] = std::pow(10.0, contrast * rng::symmetric(s));
+    });
+  } else {
+    normal_fill(seed, n, coeff);
+    for (uint64_t i = 0; i < n; ++i) coeff[i] = std::exp(coeff[i]);
+  }
+}
+}  // namespace bkg
+
 extern "C" {
 
 int bkg_stencil_size(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t* n,
@@ -136,28 +171,23 @@ int bkg_stencil_fill(int kind, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t s
   if (nx < 2 || ny < 2) return BKG_CONFIG;
   const uint64_t n = nx * ny;
   std::vector<double> coeff(n, 1.0);
-  if (kind == 1) {
-    if (!(contrast >= 0.0)) return BKG_CONFIG;
-    Rng g(seed);
-    for (double& c : coeff) c = std::pow(10.0, contrast * g.symmetric());
-  } else if (kind == 2) {
-    Rng g(seed);
-    normal_fill(g, n, coeff.data());
-    for (double& c : coeff) c = std::exp(c);
+  if (kind == 1 || kind == 2) {
+    if (kind == 1 && !(contrast >= 0.0)) return BKG_CONFIG;
+    coefficient_field(kind, seed, contrast, n, coeff.data());
   }
   assemble2d(nx, ny, coeff.data(), off, cols, vals);
   return BKG_OK;
 }
 
 int bkg_random_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out) {
-  Rng g(seed);
-  for (uint64_t i = 0; i < n * k; ++i) out[i] = g.symmetric();
+  parallel_stream(seed, n * k, 1, [=](uint64_t b, uint64_t e, uint64_t s) {
+    for (uint64_t i = b; i < e; ++i) out[i] = rng::symmetric(s);
+  });
   return BKG_OK;
 }
 
 int bkg_normal_block_rhs(uint64_t n, uint64_t k, uint64_t seed, double* out) {
-  Rng g(seed);
-  normal_fill(g, n * k, out);
+  normal_fill(seed, n * k, out);
   return BKG_OK;
 }
 

@@ -67,6 +67,7 @@ def nccl_unique_id() -> bytes:
 class PartitionedSolver:
     def __init__(self, handle, ctx: Context, n: int, k: int, rows: Tuple[int, int], virtual: bool):
         self.handle, self.ctx, self.n, self.k = handle, ctx, n, k
+        ctx.adopt(self)
         self.rows = rows
         self.is_virtual = virtual
 

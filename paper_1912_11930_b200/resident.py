@@ -14,17 +14,31 @@ from .blockkrylov import (Context, SparseMatrix, SubalgebraConfig, _check, _dp, 
 
 
 class DeviceSolver:
-    def __init__(self, a: SparseMatrix, cfg: SubalgebraConfig, ctx: Optional[Context] = None):
+    def __init__(self, a, cfg: SubalgebraConfig, ctx: Optional[Context] = None):
+        """a: SparseMatrix, or a DeviceMatrix generated on ctx."""
         self.ctx = ctx or default_context()
         self.a, self.cfg = a, cfg
         h = C.c_void_p()
         _check(N.lib().bkg_solver_create(self.ctx.handle, a.device(self.ctx), cfg.k, cfg.p,
                                          cfg._mode_code, C.byref(h)))
         self.handle = h
+        self.ctx.adopt(self)
 
     def set_rhs(self, b: np.ndarray) -> None:
         b = np.ascontiguousarray(b, dtype=np.float64)
         _check(N.lib().bkg_solver_set_rhs(self.handle, _dp(b)))
+
+    def rhs(self) -> np.ndarray:
+        """The resident right hand side B (after set_rhs / generate_rhs)."""
+        out = np.empty((self.a.n(), self.cfg.k))
+        _check(N.lib().bkg_solver_get_rhs(self.handle, _dp(out)))
+        return out
+
+    def generate_rhs(self, distribution: str = "uniform", seed: int = 7) -> None:
+        """B generated on the device: "uniform" = random_block_rhs(n, k, seed)
+        bit for bit, "normal" = the N(0,1) stream within a few ulp."""
+        code = {"uniform": 0, "normal": 1}[distribution]
+        _check(N.lib().bkg_solver_generate_rhs(self.handle, code, seed))
 
     def run(self, tol: float = 1e-8, max_iter: int = 0, record_history: bool = False) -> N.Report:
         rep = N.Report()

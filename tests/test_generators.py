@@ -54,3 +54,29 @@ def test_poisson2d_validates_like_reference():
     a = bk.poisson2d(bk.PoissonSpec.constant(4, 4))
     assert a.n() == 16 and a.nnz() == 64
     assert a.at(5, 5) == 4.0 and a.at(5, 6) == -1.0 and a.at(0, 15) == 0.0
+
+
+# The product generators run in parallel chunks of >= 2^18 draws started from
+# jumped Xorshift64Star states (csrc/rng.h); the oracle is serial.
+@pytest.mark.parametrize("n,k", [(262143, 1), (262145, 3), (300001, 5)])
+def test_parallel_uniform_rhs_matches_serial_oracle(port, n, k):
+    assert bk.random_block_rhs(n, k, 9).tobytes() == port.random_block_rhs(n, k, 9).tobytes()
+
+
+@pytest.mark.parametrize("n,k", [(524289, 1), (200001, 5)])
+def test_parallel_normal_rhs_matches_serial_oracle(port, n, k):
+    assert bk.normal_block_rhs(n, k, 13).tobytes() == port.normal_block_rhs(n, k, 13).tobytes()
+
+
+@pytest.mark.parametrize("kind", [POISSON2D_LOGUNI, DIFFUSION2D_LOGNORMAL])
+def test_parallel_coefficient_fields_match_serial_oracle(port, kind):
+    a = bk.stencil(kind, 777, 701, 1, seed=4, contrast=1.5)  # 544,677 cells
+    rp, cols, vals = port.stencil(kind, 777, 701, 1, seed=4, contrast=1.5)
+    assert a.values().tobytes() == vals.tobytes()
+
+
+def test_jump_ahead_matches_stepping(port):
+    # position m of the stream from a jumped state == the m-th serial draw
+    full = port.random_block_rhs(1, 1_000_003, 21).ravel()
+    chunk = bk.random_block_rhs(1, 1_000_003, 21).ravel()
+    assert chunk.tobytes() == full.tobytes()
