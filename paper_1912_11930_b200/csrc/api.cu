@@ -5,6 +5,8 @@
 // is no CPU fallback; without a device every call fails with BKG_CUDA.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -280,6 +282,92 @@ void keep_spare(DevBuf<T>& spare, DevBuf<T>& src) {
   if (src.count > spare.count) spare = std::move(src);
 }
 
+// ---- sliced-ELL copy of a CSR (common.cuh SellCsr) ------------------------
+__global__ void k_sell_width(int64_t n, int R, const int64_t* __restrict__ rowptr,
+                             int64_t* __restrict__ sptr) {
+  const int64_t ns = (n + R - 1) / R;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t w = 0;
+    for (int i = 0; i < R; ++i) {
+      const int64_t r = s * R + i;
+      if (r < n) w = max(w, rowptr[r + 1] - rowptr[r]);
+    }
+    sptr[s + 1] = w * R;
+    if (s == 0) sptr[0] = 0;
+  }
+}
+
+// One warp per slice: entry (slot u, row i) <- CSR entry u of row s*R + i.
+__global__ void k_sell_fill(int64_t n, int R, const int64_t* __restrict__ rowptr,
+                            const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                            const int64_t* __restrict__ sptr, int32_t* __restrict__ scols,
+                            double* __restrict__ svals) {
+  const int64_t ns = (n + R - 1) / R;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; s < ns; s += nw) {
+    const int64_t b = sptr[s], e = sptr[s + 1];
+    for (int64_t idx = b + lane; idx < e; idx += 32) {
+      const int64_t o = idx - b;
+      const int64_t u = o / R, r = s * R + o % R;
+      double v = 0.0;
+      int32_t c = kNoCol;
+      if (r < n) {
+        const int64_t rb = rowptr[r];
+        if (u < rowptr[r + 1] - rb) {
+          v = vals[rb + u];
+          c = cols[rb + u];
+        }
+      }
+      svals[idx] = v;
+      scols[idx] = c;
+    }
+  }
+}
+
+void sell_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                const double* vals, int R, SellCsr& out, SellCsr* spare) {
+  const int64_t ns = std::max<int64_t>(1, (n + R - 1) / R);
+  if (spare && spare->sptr.count >= (size_t)ns + 1 && out.sptr.count < (size_t)ns + 1)
+    out.sptr = std::move(spare->sptr);
+  out.sptr.ensure((size_t)ns + 1);
+  {
+    int64_t nn = n;
+    int rr = R;
+    int64_t* sp = out.sptr.ptr;
+    void* args[] = {&nn, &rr, &rowptr, &sp};
+    launch(c, (const void*)&k_sell_width, elem_grid(c, ns), 256, 0, args);
+  }
+  size_t tmp_bytes = 0;
+  BKG_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, out.sptr.ptr + 1,
+                                               out.sptr.ptr + 1, (int)ns, c->stream));
+  DevBuf<char> tmp(tmp_bytes + 16);
+  BKG_CUDA_CHECK(cub::DeviceScan::InclusiveSum(tmp.ptr, tmp_bytes, out.sptr.ptr + 1,
+                                               out.sptr.ptr + 1, (int)ns, c->stream));
+  int64_t total = 0;
+  d2h(c, &total, out.sptr.ptr + ns, 1);
+  sync(c);
+  const size_t need = (size_t)std::max<int64_t>(total, 1);
+  if (spare && out.cols.count < need && spare->cols.count >= need) {
+    out.cols = std::move(spare->cols);
+    out.vals = std::move(spare->vals);
+  }
+  out.cols.ensure(need);
+  out.vals.ensure(need);
+  {
+    int64_t nn = n;
+    int rr = R;
+    const int64_t* sp = out.sptr.ptr;
+    int32_t* sc = out.cols.ptr;
+    double* sv = out.vals.ptr;
+    void* args[] = {&nn, &rr, &rowptr, &cols, &vals, &sp, &sc, &sv};
+    launch(c, (const void*)&k_sell_fill, elem_grid(c, ns * 32), 256, 0, args);
+  }
+  out.rows = R;
+  out.n = n;
+}
+
 // A device matrix is bound to the ctx that uploaded it.
 void check_owner(const bkg_ctx* ctx, const bkg_matrix* a) {
   BKG_REQUIRE(ctx && a && a->ctx == ctx, BKG_CONFIG,
@@ -392,7 +480,7 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
-      g1 = occupancy_grid(c, ft.k1, ft.smem_iter, n, ft.rpc_k1);
+      g1 = occupancy_grid(c, ft.k1, ft.smem_k1, n, ft.rpc_k1);
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
       k3fn = jac ? ft.k3_jac : ft.k3;
@@ -423,6 +511,16 @@ struct bkg_solver {
     a.group = 16;
     a.ctrl = dctrl();
     a.zscale = precond == BKG_PRECOND_JACOBI ? A->inv_diag.ptr : nullptr;
+    if (fast && ft.sell_rows) {
+      // sliced-ELL copy for K1, built once per matrix (never inside a graph
+      // capture: launch_chunk calls iter_args before capturing)
+      if (A->sell.rows != ft.sell_rows || A->sell.n != n)
+        sell_build(ctx, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, ft.sell_rows, A->sell,
+                   &ctx->spare_sell);
+      a.sptr = A->sell.sptr.ptr;
+      a.scols = A->sell.cols.ptr;
+      a.svals = A->sell.vals.ptr;
+    }
     return a;
   }
 
@@ -440,7 +538,7 @@ struct bkg_solver {
       IterArgs a = iter_args(with_hist);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
-      launch(ctx, ft.k1, g1, kThreads, ft.smem_iter, args);
+      launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
@@ -827,6 +925,11 @@ int bkg_matrix_destroy(bkg_matrix* m) {
       keep_spare(m->ctx->spare_rowptr, m->rowptr);
       keep_spare(m->ctx->spare_cols, m->cols);
       keep_spare(m->ctx->spare_vals, m->vals);
+      if (m->sell.cols.count > m->ctx->spare_sell.cols.count) {
+        m->ctx->spare_sell.cols = std::move(m->sell.cols);
+        m->ctx->spare_sell.vals = std::move(m->sell.vals);
+      }
+      keep_spare(m->ctx->spare_sell.sptr, m->sell.sptr);
     }
     delete m;
   });
@@ -1148,7 +1251,7 @@ int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out) 
     if (s->fast) {
       IterArgs a = s->iter_args(false);
       void* args[] = {&a};
-      launch(s->ctx, s->ft.k1, s->g1, kThreads, s->ft.smem_iter, args);
+      launch(s->ctx, s->ft.k1, s->g1, kThreads, s->ft.smem_k1, args);
     } else {
       dev_spmm(s->ctx, s->A, s->k, s->P, s->Q.ptr, nullptr, true);
     }

@@ -114,6 +114,19 @@ __device__ __forceinline__ bool stopped(const Ctrl* c) {
   return c != nullptr && *reinterpret_cast<const volatile int32_t*>(&c->done) != 0;
 }
 
+// Sliced-ELL copy of a CSR matrix for the fused K1 (kernels_k1.cuh): slices
+// of R consecutive rows, each padded to its longest row and stored slot-major
+// (entry (slot u, row i) of slice s at sptr[s] + u * R + i; padding: value 0,
+// column kNoCol), so the R rows of a K1 warp tile read each slot's values and
+// columns as one contiguous segment.  Built on device from the CSR.
+struct SellCsr {
+  int rows = 0;  // slice height R (0: not built)
+  int64_t n = 0;
+  DevBuf<int64_t> sptr;  // nslices + 1 entry offsets
+  DevBuf<int32_t> cols;
+  DevBuf<double> vals;
+};
+
 }  // namespace bkg
 
 struct bkg_matrix;
@@ -133,6 +146,7 @@ struct bkg_ctx {
   bkg::DevBuf<int64_t> spare_rowptr;
   bkg::DevBuf<int32_t> spare_cols;
   bkg::DevBuf<double> spare_vals;
+  bkg::SellCsr spare_sell;  // sliced-ELL buffers of the last destroyed matrix
   // live matrices created on this ctx (orphaned, ctx = nullptr, when the ctx
   // is destroyed first; their buffers stay valid until bkg_matrix_destroy)
   std::set<bkg_matrix*> matrices;
@@ -147,6 +161,8 @@ struct bkg_matrix {
   bkg::DevBuf<int64_t> rowptr;
   bkg::DevBuf<int32_t> cols;
   bkg::DevBuf<double> vals;
+  // sliced-ELL copy for the fused K1 (built lazily by the first fast solve)
+  mutable bkg::SellCsr sell;
   // preconditioner data (built lazily on device)
   bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)
   bkg::DevBuf<double> lu;        // ILU(0) factors on A's pattern

@@ -6,9 +6,35 @@
 #pragma once
 
 #include "kernels_fast.cuh"
-#include "kernels_mma.cuh"
+#include "kernels_k1.cuh"
+
+// K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
+#ifndef BKG_K1_IMPL
+#define BKG_K1_IMPL 1
+#endif
 
 namespace bkg {
+
+// k1_wide schedule and CSR chunk per (K, P), the measured winners on B200
+// (tools/kernel_sweep.py): C2 (32, 8) per-tile/diagonal row
+// with the gathers; C4 classical (16, 16) flat stream; C4 p = 4 and C3
+// (64, <= 4) per-tile; C5 (64, 16) per-tile, 8-slot chunks.
+#ifdef BKG_K1W_SCHED
+template <int K, int P> constexpr int k1w_sched() { return BKG_K1W_SCHED; }
+#else
+template <int K, int P>
+constexpr int k1w_sched() {
+  return (K == 16 && P == 16) ? 2 : (K == 32 || (K == 64 && P >= 8)) ? 1 : 0;
+}
+#endif
+#ifdef BKG_K1W_CH
+template <int K, int P> constexpr int k1w_chunk() { return BKG_K1W_CH; }
+#else
+template <int K, int P>
+constexpr int k1w_chunk() {
+  return (K == 64 && P < 8) ? 4 : 8;
+}
+#endif
 
 struct FastTable {
   const void* k1 = nullptr;
@@ -20,7 +46,8 @@ struct FastTable {
   const void* gram = nullptr;
   const void* norms = nullptr;
   const void* baxpy = nullptr;
-  int smem_iter = 0;   // dynamic smem of k1 / k2
+  int smem_iter = 0;   // dynamic smem of k2 / k3 (and the scalar k1)
+  int smem_k1 = 0;     // dynamic smem of k1
   int smem_gram = 0;   // dynamic smem of gram
   int smem_norms = 0;  // dynamic smem of norms
   int cpt = 1;
@@ -31,6 +58,7 @@ struct FastTable {
   int rpc_k2 = 1;     // rows per CTA pass of K2 / K3 (grid sizing)
   int rpc_k3 = 1;
   int rpc_k1 = 1;     // rows per CTA pass of K1
+  int sell_rows = 0;  // K1 reads a sliced-ELL copy with this slice height (0: CSR)
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -44,7 +72,19 @@ template <int K, int P, bool G>
 void fill_table(FastTable* t) {
   constexpr int CPT = cpt_for<P>();
   using S = FastSmem<K, P, CPT, G>;
-  if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
+  t->smem_iter = S::bytes();
+  t->smem_k1 = t->smem_iter;
+  t->e_iter = S::RED;
+  if constexpr (K % 8 == 0 && P <= 16 && BKG_K1_IMPL == 1) {  // 256-bit gathers + DMMA Gram
+    constexpr int W = K > 32 ? 32 : K;
+    constexpr int CH = k1w_chunk<K, P>();
+    using WL = WideLayout<K, P, W, 4>;
+    t->k1 = (const void*)&k1_wide<K, P, W, 4, CH, k1w_sched<K, P>(), G>;
+    t->rpc_k1 = WL::RPW * (kThreads / 32) / WL::QW;
+    t->smem_k1 = k1_wide_smem<K, P, W, 4, G>();
+    t->sell_rows = WL::RPW;
+    if (WL::RED > t->e_iter) t->e_iter = WL::RED;
+  } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;
     t->rpc_k1 = (64 / W) * (8 * W / K);  // (rows per warp tile) x (row tiles per CTA)
@@ -83,12 +123,10 @@ void fill_table(FastTable* t) {
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
   t->norms = (const void*)&k_norms_fast<K, CPT>;
   t->baxpy = (const void*)&k_baxpy_fast<K, P, CPT, G>;
-  t->smem_iter = S::bytes();
   t->smem_gram = (int)sizeof(double) * K * P;
   t->smem_norms = (int)sizeof(double) * K;
   t->cpt = CPT;
   t->rpc = Layout<K, P, CPT>::RPC;
-  t->e_iter = S::RED;
   t->e_gram = K * P;
   t->e_norms = K;
 }

@@ -186,6 +186,10 @@ struct IterArgs {
   // Jacobi in the fused loop: Z = zscale (.) R row-wise (zscale = D^-1,
   // preconditioners.hpp:109-129); nullptr for M = I.
   const double* zscale;
+  // Sliced-ELL copy of the CSR (k1_wide; slice height = its tile rows)
+  const int64_t* sptr;
+  const int32_t* scols;
+  const double* svals;
 };
 
 // Last-CTA epilogue shared by both numerics modes: norms[k] are the column

@@ -1,0 +1,308 @@
+// kernels_k1.cuh — K1 with 256-bit operand gathers: Q = A P (kernels.hpp:129-157)
+// and alpha = <<P, Q>> (kernels.hpp:59-88), last CTA: lambda = alpha^-1 rho_prev
+// (kernels.hpp:231-240).
+//
+// Row layout: a lane owns CPL = 4 consecutive columns of one row and reads
+// each CSR operand row segment as one 32-byte LDG.256, so LPR = W / 4 lanes
+// cover the warp's W columns of a row and a warp tile is RPW = 32 / LPR rows.  Compared with the 16-byte k1_tile this halves the number of lanes
+// that replicate each row's CSR stream (the replicated (value, column) loads
+// were ~40% of K1's L1->register traffic on B200, ncu) and halves the gather
+// instructions.  The Gram P^T Q over the tile is FP64 DMMA (m8n8k4, k = 4 rows
+// per MMA): the tile's P and Q rows go through a per-warp shared-memory
+// scratch into the T (operand) layout instead of warp shuffles.
+// Rows of a tile past n contribute zeros.
+#pragma once
+
+#include "kernels_mma.cuh"
+
+namespace bkg {
+
+#ifndef BKG_K1W_LD
+#define BKG_K1W_LD 0
+#endif
+__device__ __forceinline__ void ldg4(double (&d)[4], const double* p) {
+#if BKG_K1W_LD == 1
+  asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+#elif BKG_K1W_LD == 2
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+#elif BKG_K1W_LD == 3
+  asm("ld.global.nc.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
+#else
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+#endif
+      : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
+      : "l"(p));
+}
+__device__ __forceinline__ void stg4(double* p, const double* d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(d[0]), "d"(d[1]),
+               "d"(d[2]), "d"(d[3])
+               : "memory");
+}
+
+// A warp owns W columns (W = K, or 32 when K = 64: QW = K / W warps share a
+// row block) of RPW rows.
+template <int K, int P, int W, int CPL>
+struct WideLayout {
+  static constexpr int QW = K / W;                // warps per row block
+  static constexpr int LPR = W / CPL;             // lanes per row
+  static constexpr int RPW = 32 / LPR;            // rows per warp tile
+  static constexpr int H = W / 2 + 2;             // scratch: second-half column base
+  static constexpr int SS = W + 4;                // scratch row stride (doubles)
+  static constexpr int SCR = 2 * RPW * SS;        // scratch doubles per warp (P and Q)
+  static constexpr int PT = P >= 8 ? P / 8 : 1;   // 8-col tiles per p-group side
+  static constexpr int NPAIR = P >= 8 ? (W / 8) * PT : W / 8;  // Gram tile pairs per warp
+  static constexpr int NACC = 2 * NPAIR;
+  static constexpr int TPR = 32 * QW;             // grid_reduce positions
+  static constexpr int RED = TPR * NACC;
+  static_assert(CPL == 4 && K % W == 0 && 8 % QW == 0, "column split");
+  static_assert(LPR >= 1 && 32 % LPR == 0 && RPW % 4 == 0, "row split");
+  static_assert(W % 8 == 0 && P <= 16 && (P < 8 || W % P == 0), "DMMA Gram tiles");
+};
+
+// Scratch column of logical column c (0 <= c < W): each lane's two 16-byte
+// halves go to [0, W/2) and [H, H + W/2), so a quarter-warp's stores are
+// contiguous and the T-layout operand reads of 4 rows hit distinct banks.
+#ifndef BKG_K1W_SWZ
+#define BKG_K1W_SWZ 1
+#endif
+template <int W>
+__device__ __forceinline__ int scr_col(int c) {
+  if constexpr (BKG_K1W_SWZ) return ((c & 2) ? W / 2 + 2 : 0) + (c >> 2) * 2 + (c & 1);
+  return c;
+}
+
+template <int K, int P, int W, int CPL>
+__device__ __forceinline__ void wide_pair(int pi, int& at, int& bt) {
+  using L = WideLayout<K, P, W, CPL>;
+  if constexpr (P >= 8) {  // pi = tile * PT + j: partner j inside the tile's p-group
+    const int t = pi / L::PT, j = pi % L::PT;
+    at = t;
+    bt = (t / L::PT) * L::PT + j;
+  } else {  // block-diagonal 8 x 8 tiles (8/P whole p-groups each)
+    at = bt = pi;
+  }
+}
+
+// Grid totals (red[(w * 32 + lane) * NACC + pi * 2 + i], D layout) -> row-major
+// p x p blocks.
+template <int K, int P, int W, int CPL, bool GLOBAL>
+__device__ void gather_gram_wide(const double* red, double* blocks) {
+  using L = WideLayout<K, P, W, CPL>;
+  constexpr int NB = GLOBAL ? 1 : K / P;
+  for (int idx = threadIdx.x; idx < NB * P * P; idx += kThreads) {
+    const int blk = idx / (P * P), a = (idx / P) % P, b = idx % P;
+    double s = 0.0;
+    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? K / P : blk + 1;
+    for (int g = g0; g < g1; ++g) {
+      const int ca = g * P + a, cb = g * P + b;
+      const int w = ca / W, at = (ca % W) >> 3, bt = (cb % W) >> 3;
+      const int pi = P >= 8 ? at * L::PT + (bt % L::PT) : at;
+      const int lane = ((ca & 7) << 2) | ((cb & 7) >> 1), i = cb & 1;
+      s += red[(w * 32 + lane) * L::NACC + pi * 2 + i];
+    }
+    blocks[idx] = s;
+  }
+}
+
+#ifndef BKG_K1W_MINB
+#define BKG_K1W_MINB 2
+#endif
+
+// SCHED (chosen per (K, P) from B200 measurements, fast_table.cuh):
+//   0  per tile; the diagonal operand row of tile t+1 is loaded at the end of tile t
+//   1  per tile; the diagonal operand row is loaded with the tile's gathers
+//   2  flat (tile, chunk) stream (below)
+template <int K, int P, int W, int CPL, int CH, int SCHED, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_wide(IterArgs a) {
+  using L = WideLayout<K, P, W, CPL>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  if (stopped(a.ctrl)) return;
+  constexpr int LPR = L::LPR, RPW = L::RPW, SS = L::SS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rr = lane / LPR, cl = lane % LPR;
+  const int col = (warp % L::QW) * W + cl * CPL;
+  const double* Pc = a.P + col;
+  extern __shared__ double sm[];
+  double* sp = sm + warp * L::SCR;  // P rows of the tile (T-layout source)
+  double* sq = sp + RPW * SS;       // Q rows
+  double acc[L::NACC];
+#pragma unroll
+  for (int e = 0; e < L::NACC; ++e) acc[e] = 0.0;
+  const int64_t ntile = (a.n + RPW - 1) / RPW;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::QW;
+  const int64_t rstride = wstride * RPW;
+  int64_t tile = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::QW;
+  int64_t row = tile * RPW + rr;
+
+  // Sliced-ELL stream (common.cuh SellCsr, slice height RPW = the tile):
+  // slice t spans entries [sptr[t], sptr[t+1]), slot-major, so the RPW rows
+  // of a slot are one contiguous segment; the slot count is warp-uniform.
+  auto extent = [&](int64_t t, int64_t& b, int& w) {
+    b = 0;
+    w = 0;
+    if (t < ntile) {
+      b = __ldg(a.sptr + t);
+      w = (int)((__ldg(a.sptr + t + 1) - b) / RPW);
+    }
+  };
+  auto load_chunk = [&](int64_t b, int off, int w, double (&v)[CH], int (&c)[CH]) {
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const bool in = off + u < w;
+      const int64_t e = b + (int64_t)(off + u) * RPW + rr;
+      v[u] = in ? __ldg(a.svals + e) : 0.0;
+      c[u] = in ? __ldg(a.scols + e) : kNoCol;
+    }
+  };
+
+  // gathers + FMAs of one CSR chunk; inactive slots: v = 0, x = 0
+  auto gather_fma = [&](const double (&v)[CH], const int (&c)[CH], double (&q)[CPL]) {
+    double x[CH][CPL];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      if (c[u] != kNoCol) {
+        ldg4(x[u], Pc + (int64_t)c[u] * K);
+      } else {
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) x[u][t] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) q[t] = fma(v[u], x[u][t], q[t]);
+  };
+  // tile epilogue: store Q, Gram P^T Q over the tile rows (rows -> scratch ->
+  // T-layout fragments -> DMMA)
+  auto epilogue = [&](int64_t r, const double (&q)[CPL], const double (&pd)[CPL]) {
+    if (r < a.n) stg4(a.Q + r * K + col, q);
+    const int c0 = cl * CPL;
+    *reinterpret_cast<double2*>(sp + rr * SS + scr_col<W>(c0)) = make_double2(pd[0], pd[1]);
+    *reinterpret_cast<double2*>(sp + rr * SS + scr_col<W>(c0 + 2)) = make_double2(pd[2], pd[3]);
+    *reinterpret_cast<double2*>(sq + rr * SS + scr_col<W>(c0)) = make_double2(q[0], q[1]);
+    *reinterpret_cast<double2*>(sq + rr * SS + scr_col<W>(c0 + 2)) = make_double2(q[2], q[3]);
+    __syncwarp();
+#pragma unroll
+    for (int cc = 0; cc < RPW / 4; ++cc) {
+      const int sr = (4 * cc + (lane & 3)) * SS;
+#pragma unroll
+      for (int pi = 0; pi < L::NPAIR; ++pi) {
+        int at, bt;
+        wide_pair<K, P, W, CPL>(pi, at, bt);
+        double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
+        dmma(d, sp[sr + scr_col<W>(at * 8 + (lane >> 2))],
+             sq[sr + scr_col<W>(bt * 8 + (lane >> 2))]);
+        acc[2 * pi] = d[0];
+        acc[2 * pi + 1] = d[1];
+      }
+    }
+    __syncwarp();
+  };
+
+  int64_t b0, b1, b2;
+  int w0, w1, w2;
+  double v[CH], q[CPL], pd[CPL];
+  int c[CH];
+  extent(tile, b0, w0);
+  extent(tile + wstride, b1, w1);
+  load_chunk(b0, 0, w0, v, c);
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) q[t] = pd[t] = 0.0;
+  if (SCHED != 1 && row < a.n) ldg4(pd, Pc + row * K);
+  if constexpr (SCHED == 2) {
+    // Flat stream of (tile, chunk) items: the chunk of item i+1 -- the next
+    // slots of the same slice, or the first chunk of the next tile -- is in
+    // flight while item i's gathers are, so wide slices (27-point rows) cost
+    // one memory round trip per chunk.
+    extent(tile + 2 * wstride, b2, w2);
+    int64_t cb = b0;
+    int coff = 0, cw = w0;
+    while (tile < ntile) {
+      const bool last = coff + CH >= cw;
+      const int64_t nb = last ? b1 : cb;
+      const int noff = last ? 0 : coff + CH, nw = last ? w1 : cw;
+      double nv[CH];
+      int nc[CH];
+      load_chunk(nb, noff, nw, nv, nc);
+      gather_fma(v, c, q);
+      if (last) {
+        epilogue(row, q, pd);
+        tile += wstride;
+        row += rstride;
+        b0 = b1;
+        w0 = w1;
+        b1 = b2;
+        w1 = w2;
+        extent(tile + 2 * wstride, b2, w2);
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) q[t] = pd[t] = 0.0;
+        if (row < a.n) ldg4(pd, Pc + row * K);
+      }
+      cb = nb;
+      coff = noff;
+      cw = nw;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        v[u] = nv[u];
+        c[u] = nc[u];
+      }
+    }
+  } else {
+    // Per tile: the first chunk of tile t+1 and the slice extent of tile t+2
+    // are in flight while tile t's gathers are.
+    for (; tile < ntile; tile += wstride) {
+      extent(tile + 2 * wstride, b2, w2);
+      double nv[CH];
+      int nc[CH];
+      load_chunk(b1, 0, w1, nv, nc);
+      if (SCHED == 1 && row < a.n) ldg4(pd, Pc + row * K);
+      gather_fma(v, c, q);
+      for (int off = CH; off < w0; off += CH) {  // slices wider than one chunk
+        double v2[CH];
+        int c2[CH];
+        load_chunk(b0, off, w0, v2, c2);
+        gather_fma(v2, c2, q);
+      }
+      epilogue(row, q, pd);
+      row += rstride;
+      b0 = b1;
+      w0 = w1;
+      b1 = b2;
+      w1 = w2;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        v[u] = nv[u];
+        c[u] = nc[u];
+      }
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) q[t] = pd[t] = 0.0;
+      if (SCHED == 0 && row < a.n) ldg4(pd, Pc + row * K);
+    }
+  }
+  __syncthreads();  // the scratch is reused as the reduction buffer
+  double* red = sm;
+  if (!grid_reduce<L::TPR, L::NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group))
+    return;
+  double* alpha = sm + L::RED;
+  double* ws = alpha + 3 * S::CS;
+  gather_gram_wide<K, P, W, CPL, GLOBAL>(red, alpha);
+  __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
+    return;
+  }
+  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
+}
+
+// Dynamic shared memory of k1_wide: max(warp scratch, reduction epilogue).
+template <int K, int P, int W, int CPL, bool GLOBAL>
+int k1_wide_smem() {
+  using L = WideLayout<K, P, W, CPL>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  const int scratch = (kThreads / 32) * L::SCR;
+  const int epi = L::RED + 3 * S::CS + bsolve_ws_doubles(P, kThreads) + K;
+  return (int)sizeof(double) * (scratch > epi ? scratch : epi);
+}
+
+}  // namespace bkg

@@ -149,6 +149,7 @@ struct Part {
   DevBuf<int64_t> rowptr;
   DevBuf<int32_t> cols;  // local columns: global - r0 (negative for ghost rows below)
   DevBuf<double> vals;
+  SellCsr sell;          // sliced-ELL copy for k1_wide (built at setup)
   DevBuf<double> B, X, R, Q, Pext, coef, limits, hist, red1, red2, partials, gpart, tmp;
   DevBuf<char> ctrl_buf;
   double* P = nullptr;  // own rows inside Pext
@@ -241,12 +242,14 @@ struct bkg_psolver {
       pt.tmp.alloc((size_t)cs + k);
       pt.ctrl_buf.alloc(sizeof(Ctrl));
       BKG_CUDA_CHECK(cudaMemsetAsync(pt.ctrl_buf.ptr, 0, sizeof(Ctrl), ctx->stream));
-      pt.g1 = occupancy_grid(ctx, ft.k1, ft.smem_iter, pt.nloc, ft.rpc_k1);
+      pt.g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, pt.nloc, ft.rpc_k1);
       pt.g2 = occupancy_grid(ctx, ft.k2, ft.smem_iter, pt.nloc, ft.rpc_k2);
       pt.g3 = occupancy_grid(ctx, ft.k3, ft.smem_iter, pt.nloc, ft.rpc_k3);
       const int gmax = std::max(std::max(pt.g1, pt.g2), pt.g3);
       pt.partials.alloc((size_t)gmax * ft.e_iter);
       pt.gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
+      if (ft.sell_rows)
+        sell_build(ctx, pt.nloc, pt.rowptr.ptr, pt.cols.ptr, pt.vals.ptr, ft.sell_rows, pt.sell);
     }
     if (!use_nccl) {
       std::vector<double*> r1, r2, t;
@@ -333,6 +336,9 @@ struct bkg_psolver {
     a.dist = 1;
     a.red1 = pt.red1.ptr;
     a.red2 = pt.red2.ptr;
+    a.sptr = pt.sell.sptr.ptr;
+    a.scols = pt.sell.cols.ptr;
+    a.svals = pt.sell.vals.ptr;
     return a;
   }
 
@@ -341,7 +347,7 @@ struct bkg_psolver {
     for (Part& pt : parts) {
       IterArgs a = args_of(pt, with_hist);
       void* args[] = {&a};
-      launch(ctx, ft.k1, pt.g1, kThreads, ft.smem_iter, args);
+      launch(ctx, ft.k1, pt.g1, kThreads, ft.smem_k1, args);
     }
     allreduce([](Part& q) -> DevBuf<double>& { return q.red1; }, red1_ptrs, 2 * cs);
     const int smem = (int)sizeof(double) * (bsolve_ws_doubles(p, 256) + k);
