@@ -122,11 +122,18 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms, bool
 // R -= Q lambda; rho = <<Z, R>> (Z = D^-1 R for Jacobi, R for M = I);
 // ||R_s||^2; last CTA: beta, history, stop.
 // Resident CTAs per SM (register cap) for the DMMA K2/K3, measured on B200
-// (tools/kernel_sweep.py): P = 8 tiles are small enough for 4 CTAs (64 regs);
-// at P = 16, K2 peaks at 3 and K3 (two coefficient blocks) at 2.
+// (tools/kernel_sweep.py): P = 8 K3 tiles are small enough for 4 CTAs (64
+// regs), the two-block-unrolled P <= 8 K2 runs 3; at P = 16, K2 peaks at 3
+// and K3 (two coefficient blocks) at 2.
+// K2 with P <= 8 processes two row blocks per warp step (3 CTAs/SM): C2 K2
+// 0.281 -> 0.265 ms; at P = 16 the doubled tile costs more than it hides.
+template <int P>
+constexpr int k2_unroll() {
+  return P <= 8 ? 2 : 1;
+}
 template <int P, int KERNEL>
 constexpr int mma_minb() {
-  return P <= 8 ? 4 : (KERNEL == 2 ? 3 : 2);
+  return P <= 8 ? (KERNEL == 2 ? 3 : 4) : (KERNEL == 2 ? 3 : 2);
 }
 template <int K, int P, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs a) {
@@ -147,55 +154,70 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
   const int col_a = g * L::PE + (lane & 3);            // A-fragment column base
   const int col_c = g * L::PE + 2 * (lane & 3);        // C-fragment column base
-  for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
-       rb += wstride) {
-    const int64_t row = rb * 8 + (lane >> 2);
-    const bool ok = row < a.n;
-    double qa[L::KC], rc[L::NT][2], dt[2] = {1.0, 1.0};
+  // U row blocks per warp step: all their loads are issued before any DMMA
+  // (bytes in flight per warp x U; K2 is latency-bound at U = 1)
+  constexpr int U = k2_unroll<P>();
+  for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
+       rb0 += U * wstride) {
+    double qa[U][L::KC], rc[U][L::NT][2], dt[U][2];
 #pragma unroll
-    for (int kc = 0; kc < L::KC; ++kc) qa[kc] = ok ? __ldg(a.Q + row * K + col_a + kc * 4) : 0.0;
-    if constexpr (JAC) {  // Jacobi scale of the T-layout rows 4c + (lane & 3)
+    for (int u = 0; u < U; ++u) {
+      const int64_t rb = rb0 + u * wstride;
+      const int64_t row = rb * 8 + (lane >> 2);
+      const bool ok = rb < nrb && row < a.n;
+      dt[u][0] = dt[u][1] = 1.0;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int64_t rt = rb * 8 + 4 * c + (lane & 3);
-        dt[c] = rt < a.n ? __ldg(a.zscale + rt) : 0.0;
+      for (int kc = 0; kc < L::KC; ++kc)
+        qa[u][kc] = ok ? __ldg(a.Q + row * K + col_a + kc * 4) : 0.0;
+      if constexpr (JAC) {  // Jacobi scale of the T-layout rows 4c + (lane & 3)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int64_t rt = rb * 8 + 4 * c + (lane & 3);
+          dt[u][c] = (rb < nrb && rt < a.n) ? __ldg(a.zscale + rt) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) {
+        double t[2] = {0.0, 0.0};
+        if (ok) ld_rw<2>(t, a.R + row * K + col_c + nt * 8);
+        rc[u][nt][0] = t[0];
+        rc[u][nt][1] = t[1];
       }
     }
 #pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) {
-      double t[2] = {0.0, 0.0};
-      if (ok) ld_rw<2>(t, a.R + row * K + col_c + nt * 8);
-      rc[nt][0] = t[0];
-      rc[nt][1] = t[1];
-    }
+    for (int u = 0; u < U; ++u) {
+      const int64_t rb = rb0 + u * wstride;
+      const int64_t row = rb * 8 + (lane >> 2);
+      const bool ok = rb < nrb && row < a.n;
 #pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt)
+      for (int nt = 0; nt < L::NT; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < L::KC; ++kc) dmma(rc[nt], qa[kc], nlam[kc][nt]);
+        for (int kc = 0; kc < L::KC; ++kc) dmma(rc[u][nt], qa[u][kc], nlam[kc][nt]);
 #pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) {
-      if (ok) st<2>(a.R + row * K + col_c + nt * 8, rc[nt]);
-      acc[NG + nt * 2] = fma(rc[nt][0], rc[nt][0], acc[NG + nt * 2]);
-      acc[NG + nt * 2 + 1] = fma(rc[nt][1], rc[nt][1], acc[NG + nt * 2 + 1]);
-    }
-    double tr[L::NT][2], tz[L::NT][2];
-#pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) {
-      d_to_t(rc[nt], tr[nt], lane);
-      tz[nt][0] = JAC ? tr[nt][0] * dt[0] : tr[nt][0];  // rho = <<Z, R>>
-      tz[nt][1] = JAC ? tr[nt][1] * dt[1] : tr[nt][1];
-    }
-#pragma unroll
-    for (int at = 0; at < L::NT; ++at)
-#pragma unroll
-      for (int bt = 0; bt < L::NT; ++bt) {
-        double* gacc = acc + (at * L::NT + bt) * 2;
-        double d[2] = {gacc[0], gacc[1]};
-        dmma(d, tz[at][0], tr[bt][0]);
-        dmma(d, tz[at][1], tr[bt][1]);
-        gacc[0] = d[0];
-        gacc[1] = d[1];
+      for (int nt = 0; nt < L::NT; ++nt) {
+        if (ok) st<2>(a.R + row * K + col_c + nt * 8, rc[u][nt]);
+        acc[NG + nt * 2] = fma(rc[u][nt][0], rc[u][nt][0], acc[NG + nt * 2]);
+        acc[NG + nt * 2 + 1] = fma(rc[u][nt][1], rc[u][nt][1], acc[NG + nt * 2 + 1]);
       }
+      double tr[L::NT][2], tz[L::NT][2];
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) {
+        d_to_t(rc[u][nt], tr[nt], lane);
+        tz[nt][0] = JAC ? tr[nt][0] * dt[u][0] : tr[nt][0];  // rho = <<Z, R>>
+        tz[nt][1] = JAC ? tr[nt][1] * dt[u][1] : tr[nt][1];
+      }
+#pragma unroll
+      for (int at = 0; at < L::NT; ++at)
+#pragma unroll
+        for (int bt = 0; bt < L::NT; ++bt) {
+          double* gacc = acc + (at * L::NT + bt) * 2;
+          double d[2] = {gacc[0], gacc[1]};
+          dmma(d, tz[at][0], tr[bt][0]);
+          dmma(d, tz[at][1], tr[bt][1]);
+          gacc[0] = d[0];
+          gacc[1] = d[1];
+        }
+    }
   }
   extern __shared__ double sm[];
   double* red = sm;
