@@ -378,10 +378,29 @@ void check_owner(const bkg_ctx* ctx, const bkg_matrix* a) {
 
 using namespace bkg;
 
-// Preconditioners the fused fast loop runs (identity; Jacobi is a row scale
-// folded into K2/K3).  ILU(0) uses the unfused reference-order sequence.
+// Preconditioners the fused fast loop runs: identity, Jacobi (a row scale
+// folded into K2/K3), and ILU(0) as K2a + sync-free sweeps + Gram + finish.
 static bool fused_precond(int precond) {
-  return precond == BKG_PRECOND_IDENTITY || precond == BKG_PRECOND_JACOBI;
+  return precond == BKG_PRECOND_IDENTITY || precond == BKG_PRECOND_JACOBI ||
+         precond == BKG_PRECOND_ILU0;
+}
+
+// ILU(0) loop, after the Gram rho = <<Z, R>> (coef + 3cs): beta = rho_prev^-1
+// rho, history row, stop test (the K2 epilogue of the M = I loop).
+__global__ void k_ilu_finish(Ctrl* ctrl, int nblk, int p, int k, double* coef, int cs,
+                             const double* nsq, const double* limits, double* hist, int ring) {
+  if (stopped(ctrl)) return;
+  extern __shared__ double ws[];
+  double* norms = ws + bsolve_ws_doubles(p, blockDim.x);
+  const int bad = cta_bsolve<0>(nblk, p, coef + cs, coef + 3 * cs, coef + 2 * cs, ws);
+  if (threadIdx.x == 0) ctrl->xpending = 1;
+  if (bad >= 0) {
+    record_breakdown(ctrl, bad, 2);
+    return;
+  }
+  for (int c = threadIdx.x; c < k; c += blockDim.x) norms[c] = sqrt(nsq[c]);
+  __syncthreads();
+  finish_iteration(ctrl, norms, limits, hist, ring, k);
 }
 
 // =========================================================== solver =====
@@ -397,6 +416,8 @@ struct bkg_solver {
   int g1 = 1, g2 = 1, g3 = 1;
   const void* k2fn = nullptr;  // ft.k2 / ft.k2_jac (Jacobi folded into the loop)
   const void* k3fn = nullptr;
+  int g2i = 1, gg = 1;          // ILU(0) loop: k2_ilu and Gram grids
+  DevBuf<double> ilu_nsq;       // ILU(0) loop: ||R_s||^2 from k2_ilu
   int ring = 66, chunk = 32;
   DevBuf<double> B, X, R, Q, Pb, Zb, coef, limits, hist, norms, partials, gpart;
   DevBuf<char> ctrl_buf;
@@ -468,7 +489,7 @@ struct bkg_solver {
     R.alloc(nk);
     Q.alloc(nk);
     Pb.alloc(nk);
-    if (!fast) Zb.alloc(nk);
+    if (!fast || pc == BKG_PRECOND_ILU0) Zb.alloc(nk);
     P = Pb.ptr;
     Z = Zb.ptr;
     coef.alloc((size_t)6 * cs);
@@ -483,10 +504,16 @@ struct bkg_solver {
       g1 = occupancy_grid(c, ft.k1, ft.smem_k1, n, ft.rpc_k1);
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
-      k3fn = jac ? ft.k3_jac : ft.k3;
+      k3fn = jac ? ft.k3_jac : (precond == BKG_PRECOND_ILU0 ? ft.k3_ilu : ft.k3);
       g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, ft.rpc_k2);
       g3 = occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3);
-      const int gmax = std::max(std::max(g1, g2), g3);
+      int gmax = std::max(std::max(g1, g2), g3);
+      if (precond == BKG_PRECOND_ILU0) {
+        g2i = occupancy_grid(c, ft.k2_ilu, ft.smem_iter, n, ft.rpc);
+        gg = occupancy_grid(c, ft.gram, ft.smem_gram, n, ft.rpc);
+        ilu_nsq.alloc(k);
+        gmax = std::max(gmax, std::max(g2i, gg));
+      }
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
     }
@@ -511,6 +538,7 @@ struct bkg_solver {
     a.group = 16;
     a.ctrl = dctrl();
     a.zscale = precond == BKG_PRECOND_JACOBI ? A->inv_diag.ptr : nullptr;
+    a.zsrc = precond == BKG_PRECOND_ILU0 ? Z : nullptr;
     if (fast && ft.sell_rows) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
       // capture: launch_chunk calls iter_args before capturing)
@@ -534,6 +562,50 @@ struct bkg_solver {
       const int i = fine ? fine_i : coarse;
       if (ev && i >= 0) BKG_CUDA_CHECK(cudaEventRecord(ev[i], ctx->stream));
     };
+    if (fast && precond == BKG_PRECOND_ILU0) {
+      // K1 | K2a (R -= Q lambda, norms) | sync-free ILU(0) sweeps Z = M^-1 R |
+      // rho = <<Z, R>> + finish (beta, history, stop) | K3 (P' = Z + P beta).
+      // ev: [0] [1] after K1, [2] before K3, [3] end; fine: [4] [5] around
+      // the sweeps.
+      IterArgs a = iter_args(with_hist);
+      a.red2 = ilu_nsq.ptr;
+      void* args[] = {&a};
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
+      launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
+      launch(ctx, ft.k2_ilu, g2i, kThreads, ft.smem_iter, args);
+      if (ev && fine) BKG_CUDA_CHECK(cudaEventRecord(ev[4], ctx->stream));
+      ilu_apply_sf(ctx, const_cast<bkg_matrix*>(A), k, R.ptr, Q.ptr, Z, ctrl);  // Q is free here
+      if (ev && fine) BKG_CUDA_CHECK(cudaEventRecord(ev[5], ctx->stream));
+      {
+        VecArgs va{};
+        va.n = n;
+        va.x = Z;
+        va.y = R.ptr;
+        va.out = coef.ptr + 3 * cs;
+        va.partials = partials.ptr;
+        va.gpart = gpart.ptr;
+        va.tickets = ctrl->tickets;
+        va.ctrl = ctrl;
+        void* gargs[] = {&va};
+        launch(ctx, ft.gram, gg, kThreads, ft.smem_gram, gargs);
+      }
+      {
+        const int smem = (int)sizeof(double) * (bsolve_ws_doubles(p, 256) + k);
+        allow_smem((const void*)&k_ilu_finish, smem);
+        int nb = nblk, pp = p, kk = k, c_s = cs, rg = ring;
+        double* cf = coef.ptr;
+        const double* ns = ilu_nsq.ptr;
+        const double* lm = limits.ptr;
+        double* hs = with_hist ? hist.ptr : nullptr;
+        void* fargs[] = {&ctrl, &nb, &pp, &kk, &cf, &c_s, &ns, &lm, &hs, &rg};
+        launch(ctx, (const void*)&k_ilu_finish, 1, 256, smem, fargs);
+      }
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
+      launch(ctx, k3fn, g3, kThreads, ft.smem_iter, args);
+      if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
+      return;
+    }
     if (fast) {
       IterArgs a = iter_args(with_hist);
       void* args[] = {&a};
@@ -594,14 +666,20 @@ struct bkg_solver {
   void timed_iteration(bool with_hist) {
     if (!tev[0])
       for (auto& e : tev) BKG_CUDA_CHECK(cudaEventCreate(&e));
-    launch_iteration(with_hist, tev, !fast);
+    const bool ilu = fast && precond == BKG_PRECOND_ILU0;
+    launch_iteration(with_hist, tev, !fast || ilu);
     BKG_CUDA_CHECK(cudaEventSynchronize(tev[fast ? 3 : 8]));
     auto ms = [&](int a, int b) {
       float t = 0.f;
       BKG_CUDA_CHECK(cudaEventElapsedTime(&t, tev[a], tev[b]));
       return (double)t;
     };
-    if (fast) {
+    if (ilu) {  // K1 = bop; K2a + K3 = baxpy; sweeps = precond; Gram + finish = bdot
+      class_ms[2] += ms(0, 1);
+      class_ms[1] += ms(1, 4) + ms(2, 3);
+      class_ms[3] += ms(4, 5);
+      class_ms[0] += ms(5, 2);
+    } else if (fast) {
       class_ms[2] += ms(0, 1);
       class_ms[1] += ms(1, 3);
     } else {

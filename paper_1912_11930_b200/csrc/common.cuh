@@ -174,4 +174,8 @@ struct bkg_matrix {
   bkg::DevBuf<int32_t> level_rows;  // rows ordered by level
   std::vector<int64_t> level_ptr_fwd, level_ptr_bwd;
   bkg::DevBuf<int32_t> level_rows_bwd;
+  // sync-free ILU sweeps: the two sweeps' tickets, L^-1 r scratch (standalone
+  // applies; the fused loop uses Q)
+  bkg::DevBuf<unsigned long long> ilu_state;
+  bkg::DevBuf<double> ilu_y;
 };

@@ -42,6 +42,8 @@ struct FastTable {
   const void* k3 = nullptr;
   const void* k2_jac = nullptr;  // K2 / K3 with Jacobi folded in (Z = D^-1 R)
   const void* k3_jac = nullptr;
+  const void* k2_ilu = nullptr;  // ILU(0) loop: R -= Q lambda + norms (Gram after the sweeps)
+  const void* k3_ilu = nullptr;  // K3 with P' = Z + P beta from the sweeps' Z
   const void* spmm = nullptr;
   const void* gram = nullptr;
   const void* norms = nullptr;
@@ -113,12 +115,15 @@ void fill_table(FastTable* t) {
   if constexpr (K3_MMA) {
     t->k3 = (const void*)&k3_mma<K, P, G>;
     t->k3_jac = (const void*)&k3_mma<K, P, G, true>;
+    t->k3_ilu = (const void*)&k3_mma<K, P, G, false, true>;
     t->rpc_k3 = RPC_MMA;
   } else {
     t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
     t->k3_jac = (const void*)&k3_update_xp<K, P, CPT, G, true>;
+    t->k3_ilu = (const void*)&k3_update_xp<K, P, CPT, G, false, true>;
     t->rpc_k3 = Layout<K, P, CPT>::RPC;
   }
+  t->k2_ilu = (const void*)&k2_ilu<K, P, CPT, G>;
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
   t->norms = (const void*)&k_norms_fast<K, CPT>;

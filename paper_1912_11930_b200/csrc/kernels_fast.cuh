@@ -186,6 +186,9 @@ struct IterArgs {
   // Jacobi in the fused loop: Z = zscale (.) R row-wise (zscale = D^-1,
   // preconditioners.hpp:109-129); nullptr for M = I.
   const double* zscale;
+  // ILU(0) in the fused loop: Z = M^-1 R from the sync-free sweeps (K3's
+  // P' = Z + P beta source); nullptr otherwise.
+  const double* zsrc;
   // Sliced-ELL copy of the CSR (k1_wide; slice height = its tile rows)
   const int64_t* sptr;
   const int32_t* scols;
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
 // X += P lambda (always, once K2 ran: solver.hpp:171-175 precede the beta
 // solve and the stop test); unless the solve stopped: P = Z + P beta in
 // place (solver.hpp:186-190) and rho_prev' = <<P', R>> for the next K1.
-template <int K, int P, int CPT, bool GLOBAL, bool JAC = false>
+template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false>
 __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
@@ -517,26 +520,28 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   const int64_t r1 = a.n;
   for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
        base += (int64_t)gridDim.x * L::RPC * U) {
-    double pv[U][CPT], xv[U][CPT], rv[U][CPT], dz[U];
+    double pv[U][CPT], xv[U][CPT], rv[U][CPT], zv[U][CPT], dz[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = base + u * L::RPC + slot;
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) pv[u][j] = xv[u][j] = rv[u][j] = 0.0;
+      for (int j = 0; j < CPT; ++j) pv[u][j] = xv[u][j] = rv[u][j] = zv[u][j] = 0.0;
       dz[u] = 1.0;
       if (row < r1) {
         ld_rw<CPT>(pv[u], a.P + row * K + col0);
         ld_rw<CPT>(xv[u], a.X + row * K + col0);
         if (!fin) ld_nc<CPT>(rv[u], a.R + row * K + col0);
+        if constexpr (ZS)
+          if (!fin) ld_nc<CPT>(zv[u], a.zsrc + row * K + col0);
         if constexpr (JAC)
           if (!fin) dz[u] = __ldg(a.zscale + row);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      double pn[CPT];  // Z = D^-1 R (Jacobi) or R
+      double pn[CPT];  // Z = M^-1 R: D^-1 R (Jacobi), the ILU sweeps' Z, or R
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) pn[j] = JAC ? rv[u][j] * dz[u] : rv[u][j];
+      for (int j = 0; j < CPT; ++j) pn[j] = ZS ? zv[u][j] : (JAC ? rv[u][j] * dz[u] : rv[u][j]);
 #pragma unroll
       for (int s = 0; s < L::GT; ++s) {
 #pragma unroll
@@ -577,6 +582,54 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   if (threadIdx.x == 0) a.ctrl->xpending = 0;  // every CTA has read it (we are last)
 }
 
+// ------------------------------------------------------- K2 (ILU(0)) ---
+// ILU(0) in the fused loop, first half of K2: R -= Q lambda and ||R_s||^2.
+// The Gram rho = <<Z, R>> needs Z = M^-1 R of the whole new R, so it runs
+// after the sync-free sweeps (k_gram_fast), then k_ilu_finish (beta, history,
+// stop test).  The last CTA writes the column sums of squares to a.red2.
+template <int K, int P, int CPT, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_ilu(IterArgs a) {
+  using L = Layout<K, P, CPT>;
+  using S = FastSmem<K, P, CPT, GLOBAL>;
+  if (stopped(a.ctrl)) return;
+  extern __shared__ double sm[];
+  double* lam = sm + S::RED;
+  for (int i = threadIdx.x; i < S::CS; i += kThreads) lam[i] = a.coef[i];
+  __syncthreads();
+  double acc[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
+  const int tid = threadIdx.x, pos = tid % L::TPR, slot = tid / L::TPR, lane = tid & 31;
+  const int col0 = pos * CPT;
+  const int gbase = (lane / L::GT) * L::GT;
+  const double* lg = lam + (GLOBAL ? 0 : col0 / P) * P * P;
+  for (int64_t row = (int64_t)blockIdx.x * L::RPC + slot; row - slot < a.n;
+       row += (int64_t)gridDim.x * L::RPC) {
+    const bool ok = row < a.n;
+    double qv[CPT], rv[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) qv[j] = rv[j] = 0.0;
+    if (ok) {
+      ld_nc<CPT>(qv, a.Q + row * K + col0);
+      ld_rw<CPT>(rv, a.R + row * K + col0);
+    }
+#pragma unroll
+    for (int s = 0; s < L::GT; ++s)
+#pragma unroll
+      for (int jj = 0; jj < CPT; ++jj) {
+        const double qs = __shfl_sync(kFull, qv[jj], gbase + s);
+        const int b = s * CPT + jj;
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) rv[j] = fma(-qs, lg[b * P + (col0 + j) % P], rv[j]);
+      }
+    if (ok) st<CPT>(a.R + row * K + col0, rv);
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = fma(rv[j], rv[j], acc[j]);
+  }
+  if (!grid_reduce<L::TPR, CPT>(acc, sm, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
+  for (int c = threadIdx.x; c < K; c += kThreads) a.red2[c] = sm[c];
+}
+
 // ------------------------------------------------ standalone fast kernels ----
 struct VecArgs {
   int64_t n;
@@ -591,6 +644,7 @@ struct VecArgs {
   double* gpart;
   uint32_t* tickets;
   int group;
+  const Ctrl* ctrl;  // solver loop: skip once the device stop flag is set
 };
 
 // Y = A X (kernels.hpp:129-157), FMA, CSR order.
@@ -619,6 +673,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_fast(VecArgs a) {
 template <int K, int P, int CPT, bool GLOBAL>
 __global__ void __launch_bounds__(kThreads) k_gram_fast(VecArgs a) {
   using L = Layout<K, P, CPT>;
+  if (stopped(a.ctrl)) return;
   constexpr int NACC = P * CPT;
   double acc[NACC];
 #pragma unroll

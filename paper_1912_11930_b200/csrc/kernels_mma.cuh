@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
 
 // ------------------------------------------------------------ K3 (DMMA) --
 // X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
-template <int K, int P, bool GLOBAL, bool JAC = false>
+template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
@@ -273,25 +273,36 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
        rb += wstride) {
     const int64_t row = rb * 8 + (lane >> 2);
     const bool ok = row < a.n;
-    double pa[L::KC], xc[L::NT][2], pn[L::NT][2];
+    double pa[L::KC], xc[L::NT][2], pn[L::NT][2], zz[L::NT][2];
 #pragma unroll
     for (int kc = 0; kc < L::KC; ++kc) pa[kc] = ok ? a.P[row * K + col_a + kc * 4] : 0.0;
 #pragma unroll
     for (int nt = 0; nt < L::NT; ++nt) {
-      double t[2] = {0.0, 0.0}, r[2] = {0.0, 0.0};
+      double t[2] = {0.0, 0.0}, r[2] = {0.0, 0.0}, zt[2] = {0.0, 0.0};
       if (ok) {
         ld_rw<2>(t, a.X + row * K + col_c + nt * 8);
         if (!fin) ld_nc<2>(r, a.R + row * K + col_c + nt * 8);
+        if constexpr (ZS)
+          if (!fin) ld_nc<2>(zt, a.zsrc + row * K + col_c + nt * 8);
       }
       xc[nt][0] = t[0];
       xc[nt][1] = t[1];
       pn[nt][0] = r[0];
       pn[nt][1] = r[1];
+      zz[nt][0] = zt[0];
+      zz[nt][1] = zt[1];
     }
     double tr[L::NT][2];
     if (!fin) {
 #pragma unroll
       for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tr[nt], lane);  // R, T layout
+      if constexpr (ZS) {  // P' = Z + P beta with Z from the ILU(0) sweeps
+#pragma unroll
+        for (int nt = 0; nt < L::NT; ++nt) {
+          pn[nt][0] = zz[nt][0];
+          pn[nt][1] = zz[nt][1];
+        }
+      }
       if constexpr (JAC) {  // P' = Z + P beta with Z = D^-1 R (Jacobi)
         const double dz = ok ? __ldg(a.zscale + row) : 0.0;
 #pragma unroll

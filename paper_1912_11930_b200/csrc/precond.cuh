@@ -122,6 +122,105 @@ __global__ void k_ilu_bwd_level(const Ctrl* ctrl, const int32_t* __restrict__ ro
   }
 }
 
+// ---------------------------------------------- ILU(0), sync-free sweeps --
+// One persistent launch per triangular sweep instead of one launch per
+// dependency level (C2: 382 + 382 levels, launch-bound at ~8 ms per apply).
+// Rows are cut into segments of S consecutive rows, handed to warps by an
+// atomic ticket in processing order (forward: ascending rows, backward:
+// descending); a warp sweeps its segment row by row.  Completion is carried
+// by the data itself: the output buffer is filled with a NaN sentinel before
+// the sweep, and a dependency is ready once its element is no longer the
+// sentinel (each element is one 8-byte store, read back with L2 loads), so
+// there are no fences or flags; the previous row of the segment (the x
+// neighbour of a lexicographic stencil) is taken from registers.  Every
+// dependency of the lowest unfinished row is finished and its segment's warp
+// is running, so the sweep cannot deadlock.  Lanes own columns (lane, lane +
+// 32); each element runs exactly the reference's operation sequence (CSR
+// order, unfused mul/sub), so the result is bit-identical to
+// preconditioners.hpp:95-127 (a result whose bits equal the sentinel -- a
+// NaN -- is stored as the canonical NaN).
+constexpr unsigned long long kIluSentinel = 0x7FF4DEAD7FF4DEADull;
+
+__device__ __forceinline__ double ld_ready(const double* p) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  } while (v == kIluSentinel);
+  return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ double not_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kIluSentinel ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
+
+__global__ void k_ilu_fill(const Ctrl* ctrl, int64_t total, double* a, double* b,
+                           unsigned long long* tickets) {
+  if (stopped(ctrl)) return;
+  const double s = __longlong_as_double((long long)kIluSentinel);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    a[i] = s;
+    b[i] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2) tickets[threadIdx.x] = 0;
+}
+
+// FWD: out = L^-1 src (unit lower); BWD: out = U^-1 src.  out must hold the
+// sentinel everywhere on entry; src and out must not alias.
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_ilu_sweep_sf(const Ctrl* ctrl, int64_t n, int k, int S,
+                                                      const int64_t* __restrict__ rowptr,
+                                                      const int32_t* __restrict__ cols,
+                                                      const double* __restrict__ lu,
+                                                      const double* __restrict__ inv_diag,
+                                                      const double* __restrict__ src, double* out,
+                                                      unsigned long long* ticket) {
+  if (stopped(ctrl)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = (n + S - 1) / S;
+  const bool c0 = lane < k, c1 = lane + 32 < k;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    const int64_t s = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+    if (s >= nseg) return;
+    const int64_t first = FWD ? s * S : n - 1 - s * S;  // first row in processing order
+    const int cnt = (int)(n - s * S < (int64_t)S ? n - s * S : (int64_t)S);
+    double p0 = 0.0, p1 = 0.0;  // previous row of the segment (registers)
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t row = FWD ? first + i : first - i;
+      const int64_t prev = FWD ? row - 1 : row + 1;
+      double a0 = 0.0, a1 = 0.0;
+      if (c0) a0 = src[row * k + lane];
+      if (c1) a1 = src[row * k + lane + 32];
+      const int64_t rb = rowptr[row], re = rowptr[row + 1];
+      for (int64_t e = FWD ? rb : re - 1; FWD ? e < re : e >= rb; FWD ? ++e : --e) {
+        const int64_t col = cols[e];
+        if (FWD ? col >= row : col <= row) break;
+        const double v = lu[e];
+        double x0 = 0.0, x1 = 0.0;
+        if (col == prev && i > 0) {
+          x0 = p0;
+          x1 = p1;
+        } else {
+          if (c0) x0 = ld_ready(out + col * k + lane);
+          if (c1) x1 = ld_ready(out + col * k + lane + 32);
+        }
+        a0 = __dsub_rn(a0, __dmul_rn(v, x0));
+        a1 = __dsub_rn(a1, __dmul_rn(v, x1));
+      }
+      if (!FWD) {
+        const double d = inv_diag[row];
+        a0 = __dmul_rn(a0, d);
+        a1 = __dmul_rn(a1, d);
+      }
+      if (c0) out[row * k + lane] = not_sentinel(a0);
+      if (c1) out[row * k + lane + 32] = not_sentinel(a1);
+      p0 = a0;
+      p1 = a1;
+    }
+  }
+}
+
 __global__ void k_copy_ctrl(const Ctrl* ctrl, int64_t total, const double* __restrict__ src,
                             double* __restrict__ dst) {
   if (stopped(ctrl)) return;
@@ -261,13 +360,60 @@ inline void precond_ready(bkg_ctx* c, bkg_matrix* a, int kind) {
   if (kind == BKG_PRECOND_ILU0) ilu_ready(c, a);
 }
 
+// Segment length of the sync-free sweeps (rows per ticket).
+#ifndef BKG_ILU_SEG
+#define BKG_ILU_SEG 128
+#endif
+
+// ILU(0) apply z = U^-1 L^-1 r with the sync-free sweeps (k <= 64); y is an
+// n x k scratch for L^-1 r (the fused loop passes Q, free between K2 and K1).
+inline void ilu_apply_sf(bkg_ctx* c, bkg_matrix* a, int k, const double* r, double* y, double* z,
+                         const Ctrl* ctrl) {
+  const int64_t n = (int64_t)a->n;
+  const int S = BKG_ILU_SEG;
+  const int64_t nseg = (n + S - 1) / S;
+  a->ilu_state.ensure(2);
+  int dev = 0, nsm = 0, per = 0;
+  BKG_CUDA_CHECK(cudaGetDevice(&dev));
+  BKG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per, (const void*)&k_ilu_sweep_sf<true>, 256, 0));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
+                                                               (nseg + 7) / 8));
+  const int64_t* rp = a->rowptr.ptr;
+  const int32_t* cl = a->cols.ptr;
+  const double* lu = a->lu.ptr;
+  const double* inv = a->inv_diag.ptr;
+  unsigned long long* st = a->ilu_state.ptr;
+  int64_t nn = n, tot = n * (int64_t)k;
+  int kk = k, ss = S;
+  {
+    void* args[] = {&ctrl, &tot, &y, &z, &st};
+    launch(c, (const void*)&k_ilu_fill, elem_grid(c, tot), 256, 0, args);
+  }
+  {
+    const double* srcp = r;
+    double* outp = y;
+    unsigned long long* tk = st;
+    void* args[] = {&ctrl, &nn, &kk, &ss, &rp, &cl, &lu, &inv, &srcp, &outp, &tk};
+    launch(c, (const void*)&k_ilu_sweep_sf<true>, grid, 256, 0, args);
+  }
+  {
+    const double* srcp = y;
+    double* outp = z;
+    unsigned long long* tk = st + 1;
+    void* args[] = {&ctrl, &nn, &kk, &ss, &rp, &cl, &lu, &inv, &srcp, &outp, &tk};
+    launch(c, (const void*)&k_ilu_sweep_sf<false>, grid, 256, 0, args);
+  }
+}
+
 // Z = M^-1 R on device (ctrl-gated inside the solver loop); returns the
 // FlopCounter increment.  r and z must not alias.
 inline uint64_t precond_apply_dev(bkg_ctx* c, bkg_matrix* a, int kind, int k, const double* r,
                                   double* z, const Ctrl* ctrl) {
   const int64_t n = (int64_t)a->n;
   int64_t tot = n * k;
-  if (kind == BKG_PRECOND_IDENTITY || kind == BKG_PRECOND_ILU0) {
+  if (kind == BKG_PRECOND_IDENTITY || (kind == BKG_PRECOND_ILU0 && k > 64)) {
     void* args[] = {&ctrl, &tot, &r, &z};
     launch(c, (const void*)&k_copy_ctrl, elem_grid(c, tot), 256, 0, args);
   }
@@ -279,6 +425,11 @@ inline uint64_t precond_apply_dev(bkg_ctx* c, bkg_matrix* a, int kind, int k, co
     int64_t nn = n;
     void* args[] = {&ctrl, &nn, &kk, &inv, &r, &z};
     launch(c, (const void*)&k_jacobi_apply, elem_grid(c, tot), 256, 0, args);
+    return precond_flops(a, kind, k);
+  }
+  if (k <= 64) {
+    a->ilu_y.ensure((size_t)n * k);
+    ilu_apply_sf(c, a, k, r, a->ilu_y.ptr, z, ctrl);
     return precond_flops(a, kind, k);
   }
   const int64_t* rp = a->rowptr.ptr;
