@@ -332,6 +332,15 @@ class SparseMatrix:
     def values(self) -> np.ndarray:
         return self.values_
 
+    def diagonal(self) -> np.ndarray:
+        """A(r, r) for every row (0 where not stored), vectorised."""
+        n = self._n
+        rows = np.repeat(np.arange(n, dtype=np.uint64), np.diff(self.row_offsets_).astype(np.int64))
+        hit = self.col_indices_ == rows
+        d = np.zeros(n)
+        d[rows[hit].astype(np.int64)] = self.values_[hit]
+        return d
+
     def at(self, row: int, col: int) -> float:
         lo, hi = int(self.row_offsets_[row]), int(self.row_offsets_[row + 1])
         i = lo + int(np.searchsorted(self.col_indices_[lo:hi], col))
@@ -478,9 +487,10 @@ class Preconditioner:
 
     @staticmethod
     def jacobi(a: SparseMatrix) -> "Preconditioner":
-        for r in range(a.n()):
-            if not a.at(r, r) > 0.0:
-                raise FactorizationError(r, f"jacobi: diagonal entry {r} is not strictly positive")
+        bad = np.flatnonzero(~(a.diagonal() > 0.0))
+        if bad.size:
+            r = int(bad[0])
+            raise FactorizationError(r, f"jacobi: diagonal entry {r} is not strictly positive")
         return Preconditioner(JACOBI, a.n(), a)
 
     def kind(self) -> str:
