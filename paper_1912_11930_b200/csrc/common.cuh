@@ -178,4 +178,13 @@ struct bkg_matrix {
   // applies; the fused loop uses Q)
   bkg::DevBuf<unsigned long long> ilu_state;
   bkg::DevBuf<double> ilu_y;
+  int ilu_lower_max = 0, ilu_upper_max = 0;  // longest strictly lower / upper row part
+  // ELL copies (D entries per row, processing order) of the factors' strict
+  // lower / upper parts; D = 0: not built (rows longer than 16: CSR sweeps)
+  bkg::DevBuf<int32_t> ilu_ell_lc, ilu_ell_uc;
+  bkg::DevBuf<double> ilu_ell_lv, ilu_ell_uv;
+  int ilu_ell_dl = 0, ilu_ell_du = 0;
+  // sync-free sweep segments (processing-order position boundaries)
+  bkg::DevBuf<int64_t> ilu_seg_f, ilu_seg_b;
+  int64_t ilu_nseg_f = 0, ilu_nseg_b = 0;
 };

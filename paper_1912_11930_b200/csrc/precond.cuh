@@ -139,6 +139,13 @@ __global__ void k_ilu_bwd_level(const Ctrl* ctrl, const int32_t* __restrict__ ro
 // order, unfused mul/sub), so the result is bit-identical to
 // preconditioners.hpp:95-127 (a result whose bits equal the sentinel -- a
 // NaN -- is stored as the canonical NaN).
+#ifndef BKG_ILU_ELL
+#define BKG_ILU_ELL 1
+#endif
+// Longest sync-free sweep segment (rows per ticket).
+#ifndef BKG_ILU_SEG
+#define BKG_ILU_SEG 256
+#endif
 constexpr unsigned long long kIluSentinel = 0x7FF4DEAD7FF4DEADull;
 
 __device__ __forceinline__ double ld_ready(const double* p) {
@@ -164,10 +171,12 @@ __global__ void k_ilu_fill(const Ctrl* ctrl, int64_t total, double* a, double* b
   if (blockIdx.x == 0 && threadIdx.x < 2) tickets[threadIdx.x] = 0;
 }
 
-// FWD: out = L^-1 src (unit lower); BWD: out = U^-1 src.  out must hold the
-// sentinel everywhere on entry; src and out must not alias.
+// FWD: out = L^-1 src (unit lower); BWD: out = U^-1 src over the CSR (rows
+// with more than 16 triangle entries); out must hold the sentinel everywhere
+// on entry; src and out must not alias.
 template <bool FWD>
-__global__ void __launch_bounds__(256) k_ilu_sweep_sf(const Ctrl* ctrl, int64_t n, int k, int S,
+__global__ void __launch_bounds__(256) k_ilu_sweep_csr(const Ctrl* ctrl, int64_t n, int k, int64_t nseg,
+                                                      const int64_t* __restrict__ segs,
                                                       const int64_t* __restrict__ rowptr,
                                                       const int32_t* __restrict__ cols,
                                                       const double* __restrict__ lu,
@@ -176,15 +185,17 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_sf(const Ctrl* ctrl, int64_t 
                                                       unsigned long long* ticket) {
   if (stopped(ctrl)) return;
   const int lane = threadIdx.x & 31;
-  const int64_t nseg = (n + S - 1) / S;
   const bool c0 = lane < k, c1 = lane + 32 < k;
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1ull);
     const int64_t s = (int64_t)__shfl_sync(0xffffffffu, t, 0);
     if (s >= nseg) return;
-    const int64_t first = FWD ? s * S : n - 1 - s * S;  // first row in processing order
-    const int cnt = (int)(n - s * S < (int64_t)S ? n - s * S : (int64_t)S);
+    // segment s: positions [segs[s], segs[s+1]) in processing order (row =
+    // position forward, n - 1 - position backward)
+    const int64_t pb = segs[s];
+    const int64_t first = FWD ? pb : n - 1 - pb;  // first row in processing order
+    const int cnt = (int)(segs[s + 1] - pb);
     double p0 = 0.0, p1 = 0.0;  // previous row of the segment (registers)
     for (int i = 0; i < cnt; ++i) {
       const int64_t row = FWD ? first + i : first - i;
@@ -217,6 +228,123 @@ __global__ void __launch_bounds__(256) k_ilu_sweep_sf(const Ctrl* ctrl, int64_t 
       if (c1) out[row * k + lane + 32] = not_sentinel(a1);
       p0 = a0;
       p1 = a1;
+    }
+  }
+}
+
+// Sweep over a padded row-major copy of the triangle (ELL: D entries per row
+// in the reference's processing order, column -1 = padding): entry addresses
+// need no row-offset load, and row i+1's entries and source element are
+// loaded while row i is computed, so a row costs one dependent load round
+// trip (its dependencies) instead of three.  Few registers: occupancy (the
+// number of segments in flight) sets the sweep's speed.
+template <bool FWD, int D>
+__global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const Ctrl* ctrl, int64_t n, int k, int64_t nseg,
+                                                       const int64_t* __restrict__ segs,
+                                                       const int32_t* __restrict__ ecols,
+                                                       const double* __restrict__ evals,
+                                                       const double* __restrict__ inv_diag,
+                                                       const double* __restrict__ src,
+                                                       double* out, unsigned long long* ticket) {
+  if (stopped(ctrl)) return;
+  // k <= 16: the warp splits into 32 / W lane groups of W = 8 or 16 lanes,
+  // each sweeping its own segment (more segments in flight per register)
+  const int W = k <= 8 ? 8 : (k <= 16 ? 16 : 32);
+  const int wl = threadIdx.x & 31, g = wl / W;
+  const int lane = wl % W;  // column index within the group
+  const unsigned gmask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << (g * W));
+  const bool c0 = lane < k, c1 = lane + 32 < k;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1ull);
+    const int64_t s = (int64_t)__shfl_sync(gmask, t, g * W);
+    if (s >= nseg) return;
+    const int64_t pb = segs[s];
+    const int64_t first = FWD ? pb : n - 1 - pb;
+    const int cnt = (int)(segs[s + 1] - pb);
+    int cc[D];
+    double vv[D], s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      cc[u] = ecols[first * D + u];
+      vv[u] = evals[first * D + u];
+    }
+    if (c0) s0 = src[first * k + lane];
+    if (c1) s1 = src[first * k + lane + 32];
+    double p0 = 0.0, p1 = 0.0;
+    for (int i = 0; i < cnt; ++i) {
+      const int64_t row = FWD ? first + i : first - i;
+      const int64_t prev = FWD ? row - 1 : row + 1;
+      int nc[D];
+      double nv[D], n0 = 0.0, n1 = 0.0;
+      if (i + 1 < cnt) {  // next row's entries and source element
+        const int64_t nr = FWD ? row + 1 : row - 1;
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+          nc[u] = ecols[nr * D + u];
+          nv[u] = evals[nr * D + u];
+        }
+        if (c0) n0 = src[nr * k + lane];
+        if (c1) n1 = src[nr * k + lane + 32];
+      }
+      double a0 = s0, a1 = s1;
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        if (cc[u] < 0) break;
+        double x0 = 0.0, x1 = 0.0;
+        if (cc[u] == prev && i > 0) {
+          x0 = p0;
+          x1 = p1;
+        } else {
+          if (c0) x0 = ld_ready(out + (int64_t)cc[u] * k + lane);
+          if (c1) x1 = ld_ready(out + (int64_t)cc[u] * k + lane + 32);
+        }
+        a0 = __dsub_rn(a0, __dmul_rn(vv[u], x0));
+        a1 = __dsub_rn(a1, __dmul_rn(vv[u], x1));
+      }
+      if (!FWD) {
+        const double d = inv_diag[row];
+        a0 = __dmul_rn(a0, d);
+        a1 = __dmul_rn(a1, d);
+      }
+      if (c0) out[row * k + lane] = not_sentinel(a0);
+      if (c1) out[row * k + lane + 32] = not_sentinel(a1);
+      p0 = a0;
+      p1 = a1;
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        cc[u] = nc[u];
+        vv[u] = nv[u];
+      }
+      s0 = n0;
+      s1 = n1;
+    }
+  }
+}
+
+// ELL copy of the strict lower (FWD, CSR order) or upper (BWD, reverse CSR
+// order) part of the ILU factors: D entries per row, column -1 = padding.
+__global__ void k_ilu_ell_build(int64_t n, int D, bool fwd, const int64_t* __restrict__ rowptr,
+                                const int32_t* __restrict__ cols, const double* __restrict__ lu,
+                                int32_t* __restrict__ ecols, double* __restrict__ evals) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int u = 0;
+    const int64_t rb = rowptr[r], re = rowptr[r + 1];
+    if (fwd) {
+      for (int64_t e = rb; e < re && cols[e] < r && u < D; ++e, ++u) {
+        ecols[r * D + u] = cols[e];
+        evals[r * D + u] = lu[e];
+      }
+    } else {
+      for (int64_t e = re - 1; e >= rb && cols[e] > r && u < D; --e, ++u) {
+        ecols[r * D + u] = cols[e];
+        evals[r * D + u] = lu[e];
+      }
+    }
+    for (; u < D; ++u) {
+      ecols[r * D + u] = -1;
+      evals[r * D + u] = 0.0;
     }
   }
 }
@@ -275,12 +403,53 @@ inline void build_levels(bkg_ctx* c, bkg_matrix* a) {
   };
   make(true, a->level_rows, a->level_ptr_fwd);
   make(false, a->level_rows_bwd, a->level_ptr_bwd);
-  // ILU multiply-add count per apply (preconditioners.hpp:123-125)
+  // ILU multiply-add count per apply (preconditioners.hpp:123-125) and the
+  // longest strictly lower / upper row parts (sync-free sweep pipeline depth)
   uint64_t off = 0;
-  for (int64_t r = 0; r < n; ++r)
-    for (int64_t i = rp[r]; i < rp[r + 1]; ++i)
+  int lmax = 0, umax = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    int lo = 0, up = 0;
+    for (int64_t i = rp[r]; i < rp[r + 1]; ++i) {
       if (cl[i] != r) ++off;
+      if (cl[i] < r) ++lo;
+      if (cl[i] > r) ++up;
+    }
+    lmax = std::max(lmax, lo);
+    umax = std::max(umax, up);
+  }
   a->ilu_offdiag = off;
+  a->ilu_lower_max = lmax;
+  a->ilu_upper_max = umax;
+  // Sync-free sweep segments: maximal runs of rows chained by the previous
+  // row (forward: row r depends on r-1; backward: on r+1), split every
+  // BKG_ILU_SEG rows, so a segment's first row never waits for the end of the
+  // segment before it (stencil x-lines become segments).
+  auto segs = [&](bool fwd, DevBuf<int64_t>& out, int64_t& count) {
+    std::vector<int64_t> b;
+    int64_t run = 0;
+    for (int64_t q = 0; q < n; ++q) {  // q: position in processing order
+      const int64_t r = fwd ? q : n - 1 - q;
+      bool chained = false;
+      if (q > 0) {
+        const int64_t want = fwd ? r - 1 : r + 1;
+        for (int64_t i = rp[r]; i < rp[r + 1]; ++i)
+          if (cl[i] == want) chained = true;
+      }
+      if (!chained || run >= BKG_ILU_SEG) {
+        b.push_back(q);
+        run = 0;
+      }
+      ++run;
+    }
+    b.push_back(n);
+    count = (int64_t)b.size() - 1;
+    out.alloc(b.size());
+    BKG_CUDA_CHECK(cudaMemcpyAsync(out.ptr, b.data(), sizeof(int64_t) * b.size(),
+                                   cudaMemcpyHostToDevice, c->stream));
+    BKG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+  };
+  segs(true, a->ilu_seg_f, a->ilu_nseg_f);
+  segs(false, a->ilu_seg_b, a->ilu_nseg_b);
 }
 
 inline int grid_for(const bkg_ctx* c, int64_t total) { return elem_grid(c, total); }
@@ -344,6 +513,28 @@ inline void ilu_ready(bkg_ctx* c, bkg_matrix* a) {
     throw Error(BKG_FACTORIZATION, "ilu0: zero pivot or missing diagonal in row " +
                                        std::to_string(h));
   }
+  // ELL copies of the factors' strict triangles for the sync-free sweeps
+  a->ilu_ell_dl = a->ilu_ell_du = 0;
+  if (BKG_ILU_ELL && a->ilu_lower_max <= 16 && a->ilu_upper_max <= 16) {
+    auto round = [](int d) { return d <= 4 ? 4 : d <= 8 ? 8 : 16; };
+    int dl = round(a->ilu_lower_max), du = round(a->ilu_upper_max);
+    a->ilu_ell_lc.ensure((size_t)n * dl);
+    a->ilu_ell_lv.ensure((size_t)n * dl);
+    a->ilu_ell_uc.ensure((size_t)n * du);
+    a->ilu_ell_uv.ensure((size_t)n * du);
+    for (int pass = 0; pass < 2; ++pass) {
+      bool fw = pass == 0;
+      int d = fw ? dl : du;
+      int32_t* ec = fw ? a->ilu_ell_lc.ptr : a->ilu_ell_uc.ptr;
+      double* ev = fw ? a->ilu_ell_lv.ptr : a->ilu_ell_uv.ptr;
+      int64_t nn = n;
+      const double* luc = a->lu.ptr;
+      void* args[] = {&nn, &d, &fw, &rp, &cl, &luc, &ec, &ev};
+      launch(c, (const void*)&k_ilu_ell_build, elem_grid(c, n), 256, 0, args);
+    }
+    a->ilu_ell_dl = dl;
+    a->ilu_ell_du = du;
+  }
   a->precond_ready = BKG_PRECOND_ILU0;
 }
 
@@ -360,9 +551,12 @@ inline void precond_ready(bkg_ctx* c, bkg_matrix* a, int kind) {
   if (kind == BKG_PRECOND_ILU0) ilu_ready(c, a);
 }
 
-// Segment length of the sync-free sweeps (rows per ticket).
+// Longest sync-free sweep segment (rows per ticket).
+#ifndef BKG_ILU_WARPS
+#define BKG_ILU_WARPS 0  // cap on concurrent sweep warps (0: one full wave)
+#endif
 #ifndef BKG_ILU_SEG
-#define BKG_ILU_SEG 128
+#define BKG_ILU_SEG 256
 #endif
 
 // ILU(0) apply z = U^-1 L^-1 r with the sync-free sweeps (k <= 64); y is an
@@ -370,40 +564,58 @@ inline void precond_ready(bkg_ctx* c, bkg_matrix* a, int kind) {
 inline void ilu_apply_sf(bkg_ctx* c, bkg_matrix* a, int k, const double* r, double* y, double* z,
                          const Ctrl* ctrl) {
   const int64_t n = (int64_t)a->n;
-  const int S = BKG_ILU_SEG;
-  const int64_t nseg = (n + S - 1) / S;
   a->ilu_state.ensure(2);
-  int dev = 0, nsm = 0, per = 0;
+  const int64_t nseg = std::max(a->ilu_nseg_f, a->ilu_nseg_b);
+  int dev = 0, nsm = 0;
   BKG_CUDA_CHECK(cudaGetDevice(&dev));
   BKG_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per, (const void*)&k_ilu_sweep_sf<true>, 256, 0));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
-                                                               (nseg + 7) / 8));
+  // as many resident warps as fit: a sweep is latency-bound per row, so the
+  // number of segments in flight sets its speed
+  auto grid_of = [&](const void* fn) {
+    int per = 0;
+    BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0));
+    int64_t cap = (int64_t)nsm * std::max(per, 1);
+    if (BKG_ILU_WARPS > 0) cap = std::min<int64_t>(cap, BKG_ILU_WARPS / 8);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (nseg + 7) / 8));
+  };
+  const bool ell = a->ilu_ell_dl > 0 && a->ilu_ell_du > 0;
+  auto ell_fn = [](bool fw, int d) -> const void* {
+    if (fw) return d <= 4 ? (const void*)&k_ilu_sweep_ell<true, 4>
+                 : d <= 8 ? (const void*)&k_ilu_sweep_ell<true, 8>
+                          : (const void*)&k_ilu_sweep_ell<true, 16>;
+    return d <= 4 ? (const void*)&k_ilu_sweep_ell<false, 4>
+         : d <= 8 ? (const void*)&k_ilu_sweep_ell<false, 8>
+                  : (const void*)&k_ilu_sweep_ell<false, 16>;
+  };
+  const void* fwd = ell ? ell_fn(true, a->ilu_ell_dl) : (const void*)&k_ilu_sweep_csr<true>;
+  const void* bwd = ell ? ell_fn(false, a->ilu_ell_du) : (const void*)&k_ilu_sweep_csr<false>;
   const int64_t* rp = a->rowptr.ptr;
   const int32_t* cl = a->cols.ptr;
   const double* lu = a->lu.ptr;
   const double* inv = a->inv_diag.ptr;
   unsigned long long* st = a->ilu_state.ptr;
   int64_t nn = n, tot = n * (int64_t)k;
-  int kk = k, ss = S;
+  int kk = k;
   {
     void* args[] = {&ctrl, &tot, &y, &z, &st};
     launch(c, (const void*)&k_ilu_fill, elem_grid(c, tot), 256, 0, args);
   }
-  {
-    const double* srcp = r;
-    double* outp = y;
-    unsigned long long* tk = st;
-    void* args[] = {&ctrl, &nn, &kk, &ss, &rp, &cl, &lu, &inv, &srcp, &outp, &tk};
-    launch(c, (const void*)&k_ilu_sweep_sf<true>, grid, 256, 0, args);
-  }
-  {
-    const double* srcp = y;
-    double* outp = z;
-    unsigned long long* tk = st + 1;
-    void* args[] = {&ctrl, &nn, &kk, &ss, &rp, &cl, &lu, &inv, &srcp, &outp, &tk};
-    launch(c, (const void*)&k_ilu_sweep_sf<false>, grid, 256, 0, args);
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool fw = pass == 0;
+    const double* srcp = fw ? r : y;
+    double* outp = fw ? y : z;
+    unsigned long long* tk = st + pass;
+    int64_t ns = fw ? a->ilu_nseg_f : a->ilu_nseg_b;
+    const int64_t* sg = fw ? a->ilu_seg_f.ptr : a->ilu_seg_b.ptr;
+    if (ell) {
+      const int32_t* ec = fw ? a->ilu_ell_lc.ptr : a->ilu_ell_uc.ptr;
+      const double* ev = fw ? a->ilu_ell_lv.ptr : a->ilu_ell_uv.ptr;
+      void* args[] = {&ctrl, &nn, &kk, &ns, &sg, &ec, &ev, &inv, &srcp, &outp, &tk};
+      launch(c, fw ? fwd : bwd, grid_of(fw ? fwd : bwd), 256, 0, args);
+    } else {
+      void* args[] = {&ctrl, &nn, &kk, &ns, &sg, &rp, &cl, &lu, &inv, &srcp, &outp, &tk};
+      launch(c, fw ? fwd : bwd, grid_of(fw ? fwd : bwd), 256, 0, args);
+    }
   }
 }
 
