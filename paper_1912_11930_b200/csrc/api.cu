@@ -380,6 +380,12 @@ using namespace bkg;
 
 // Preconditioners the fused fast loop runs: identity, Jacobi (a row scale
 // folded into K2/K3), and ILU(0) as K2a + sync-free sweeps + Gram + finish.
+// Deferred X update in the fused loop (k3 XM = 1 / 2 alternating): X is read
+// and written every other iteration; P ping-pongs between two buffers.
+#ifndef BKG_DEFER_X
+#define BKG_DEFER_X 1
+#endif
+
 static bool fused_precond(int precond) {
   return precond == BKG_PRECOND_IDENTITY || precond == BKG_PRECOND_JACOBI ||
          precond == BKG_PRECOND_ILU0;
@@ -419,7 +425,10 @@ struct bkg_solver {
   int g2i = 1, gg = 1;          // ILU(0) loop: k2_ilu and Gram grids
   DevBuf<double> ilu_nsq;       // ILU(0) loop: ||R_s||^2 from k2_ilu
   int ring = 66, chunk = 32;
-  DevBuf<double> B, X, R, Q, Pb, Zb, coef, limits, hist, norms, partials, gpart;
+  DevBuf<double> B, X, R, Q, Pb, Pb2, Zb, coef, limits, hist, norms, partials, gpart;
+  bool defer = false;         // deferred X update (fast loop without an observer)
+  int pcx = 0;                // K3 table row: 0 identity, 1 Jacobi, 2 ILU(0)
+  uint64_t iter_launched = 0; // fused iterations queued since setup (deferred-X parity)
   DevBuf<char> ctrl_buf;
   Ctrl* h_ctrl = nullptr;
   double* h_ring = nullptr;
@@ -504,9 +513,12 @@ struct bkg_solver {
       g1 = occupancy_grid(c, ft.k1, ft.smem_k1, n, ft.rpc_k1);
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
-      k3fn = jac ? ft.k3_jac : (precond == BKG_PRECOND_ILU0 ? ft.k3_ilu : ft.k3);
+      pcx = jac ? 1 : (precond == BKG_PRECOND_ILU0 ? 2 : 0);
+      k3fn = ft.k3x[pcx][0];
+      if (BKG_DEFER_X) Pb2.alloc(nk);
       g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, ft.rpc_k2);
-      g3 = occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3);
+      g3 = std::min(occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3),
+                    occupancy_grid(c, ft.k3x[pcx][2], ft.smem_iter, n, ft.rpc_k3));
       int gmax = std::max(std::max(g1, g2), g3);
       if (precond == BKG_PRECOND_ILU0) {
         g2i = occupancy_grid(c, ft.k2_ilu, ft.smem_iter, n, ft.rpc);
@@ -539,6 +551,8 @@ struct bkg_solver {
     a.ctrl = dctrl();
     a.zscale = precond == BKG_PRECOND_JACOBI ? A->inv_diag.ptr : nullptr;
     a.zsrc = precond == BKG_PRECOND_ILU0 ? Z : nullptr;
+    a.Pn = P;
+    a.Pold = nullptr;
     if (fast && ft.sell_rows) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
       // capture: launch_chunk calls iter_args before capturing)
@@ -556,6 +570,17 @@ struct bkg_solver {
   // ev (optional): 4 events around K1 | K2 | K3 (fast) or the coarse phases
   // (exact); fine = true (exact only): 9 events at the kernel-class
   // boundaries of solver.hpp:161-187 (see timed_iteration).
+  // Deferred X: even iterations (XM 1) read P from Pb and write P' to Pb2,
+  // odd ones (XM 2) read Pb2, flush X with Pb, and write P' over Pb.
+  const void* k3_for(IterArgs& a) {
+    if (!defer) return k3fn;
+    const bool odd = (iter_launched++ & 1) != 0;
+    a.P = odd ? Pb2.ptr : Pb.ptr;
+    a.Pn = odd ? Pb.ptr : Pb2.ptr;
+    a.Pold = odd ? Pb.ptr : nullptr;
+    return ft.k3x[pcx][odd ? 2 : 1];
+  }
+
   void launch_iteration(bool with_hist, cudaEvent_t* ev = nullptr, bool fine = false) {
     Ctrl* ctrl = dctrl();
     auto mark = [&](int coarse, int fine_i) {
@@ -569,6 +594,7 @@ struct bkg_solver {
       // the sweeps.
       IterArgs a = iter_args(with_hist);
       a.red2 = ilu_nsq.ptr;
+      const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
       launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
@@ -602,19 +628,20 @@ struct bkg_solver {
         launch(ctx, (const void*)&k_ilu_finish, 1, 256, smem, fargs);
       }
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
-      launch(ctx, k3fn, g3, kThreads, ft.smem_iter, args);
+      launch(ctx, k3, g3, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
       return;
     }
     if (fast) {
       IterArgs a = iter_args(with_hist);
+      const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
       launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
-      launch(ctx, k3fn, g3, kThreads, ft.smem_iter, args);
+      launch(ctx, k3, g3, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
       return;
     }
@@ -696,6 +723,8 @@ struct bkg_solver {
   // Returns true when R0 already satisfies the stop test.
   bool setup(const double* x0_host, double tol, uint64_t max_iter, bool record,
              bkg_report* rep, std::vector<double>* limits_host, bool* x0_nonzero) {
+    iter_launched = 0;
+    defer = fast && BKG_DEFER_X;
     const size_t nk = (size_t)n * k;
     precond_ready(ctx, const_cast<bkg_matrix*>(A), precond);  // FactorizationError surfaces here
     bool x0_zero = true;
@@ -864,6 +893,7 @@ struct bkg_solver {
       sync(ctx);
       cb(0, hx.data(), hr.data(), (uint64_t)n, (uint64_t)k, user);
     }
+    if (cb) defer = false;  // the observer sees X after every iteration
     loop(record, cb, user, &rep->loop_seconds);
     fill_report(rep, conv0);
     rep->seconds_bdot = 1e-3 * class_ms[0];

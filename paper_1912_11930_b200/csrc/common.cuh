@@ -95,7 +95,7 @@ struct Ctrl {
   int32_t breakdown;
   int32_t stage;       // 0 normal; 1 lambda-breakdown; 2 beta-breakdown
   int32_t xpending;    // fast mode: K2 ran, K3 still owes X += P lambda
-  int32_t pad_;
+  int32_t xold;        // deferred X: the previous iteration's X += P lambda is pending
   uint64_t iterations; // completed iterations
   uint64_t max_iter;
   uint64_t breakdown_iteration;

@@ -44,6 +44,8 @@ struct FastTable {
   const void* k3_jac = nullptr;
   const void* k2_ilu = nullptr;  // ILU(0) loop: R -= Q lambda + norms (Gram after the sweeps)
   const void* k3_ilu = nullptr;  // K3 with P' = Z + P beta from the sweeps' Z
+  // K3 by [preconditioner: identity, Jacobi, ILU(0)][deferred-X mode 0/1/2]
+  const void* k3x[3][3] = {};
   const void* spmm = nullptr;
   const void* gram = nullptr;
   const void* norms = nullptr;
@@ -113,17 +115,32 @@ void fill_table(FastTable* t) {
     t->rpc_k2 = Layout<K, P, CPT>::RPC;
   }
   if constexpr (K3_MMA) {
-    t->k3 = (const void*)&k3_mma<K, P, G>;
-    t->k3_jac = (const void*)&k3_mma<K, P, G, true>;
-    t->k3_ilu = (const void*)&k3_mma<K, P, G, false, true>;
+    t->k3x[0][0] = (const void*)&k3_mma<K, P, G>;
+    t->k3x[0][1] = (const void*)&k3_mma<K, P, G, false, false, 1>;
+    t->k3x[0][2] = (const void*)&k3_mma<K, P, G, false, false, 2>;
+    t->k3x[1][0] = (const void*)&k3_mma<K, P, G, true>;
+    t->k3x[1][1] = (const void*)&k3_mma<K, P, G, true, false, 1>;
+    t->k3x[1][2] = (const void*)&k3_mma<K, P, G, true, false, 2>;
+    t->k3x[2][0] = (const void*)&k3_mma<K, P, G, false, true>;
+    t->k3x[2][1] = (const void*)&k3_mma<K, P, G, false, true, 1>;
+    t->k3x[2][2] = (const void*)&k3_mma<K, P, G, false, true, 2>;
     t->rpc_k3 = RPC_MMA;
   } else {
-    t->k3 = (const void*)&k3_update_xp<K, P, CPT, G>;
-    t->k3_jac = (const void*)&k3_update_xp<K, P, CPT, G, true>;
-    t->k3_ilu = (const void*)&k3_update_xp<K, P, CPT, G, false, true>;
+    t->k3x[0][0] = (const void*)&k3_update_xp<K, P, CPT, G>;
+    t->k3x[0][1] = (const void*)&k3_update_xp<K, P, CPT, G, false, false, 1>;
+    t->k3x[0][2] = (const void*)&k3_update_xp<K, P, CPT, G, false, false, 2>;
+    t->k3x[1][0] = (const void*)&k3_update_xp<K, P, CPT, G, true>;
+    t->k3x[1][1] = (const void*)&k3_update_xp<K, P, CPT, G, true, false, 1>;
+    t->k3x[1][2] = (const void*)&k3_update_xp<K, P, CPT, G, true, false, 2>;
+    t->k3x[2][0] = (const void*)&k3_update_xp<K, P, CPT, G, false, true>;
+    t->k3x[2][1] = (const void*)&k3_update_xp<K, P, CPT, G, false, true, 1>;
+    t->k3x[2][2] = (const void*)&k3_update_xp<K, P, CPT, G, false, true, 2>;
     t->rpc_k3 = Layout<K, P, CPT>::RPC;
   }
   t->k2_ilu = (const void*)&k2_ilu<K, P, CPT, G>;
+  t->k3 = t->k3x[0][0];
+  t->k3_jac = t->k3x[1][0];
+  t->k3_ilu = t->k3x[2][0];
   t->spmm = (const void*)&k_spmm_fast<K, CPT>;
   t->gram = (const void*)&k_gram_fast<K, P, CPT, G>;
   t->norms = (const void*)&k_norms_fast<K, CPT>;

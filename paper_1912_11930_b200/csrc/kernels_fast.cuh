@@ -193,6 +193,10 @@ struct IterArgs {
   const int64_t* sptr;
   const int32_t* scols;
   const double* svals;
+  // Deferred X update (K3 template XM): K3 writes P' to Pn; in a flush
+  // launch X += Pold lambda_old + P lambda (lambda_old at coef + 4 cs).
+  double* Pn;
+  const double* Pold;
 };
 
 // Last-CTA epilogue shared by both numerics modes: norms[k] are the column
@@ -491,19 +495,26 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
 // X += P lambda (always, once K2 ran: solver.hpp:171-175 precede the beta
 // solve and the stop test); unless the solve stopped: P = Z + P beta in
 // place (solver.hpp:186-190) and rho_prev' = <<P', R>> for the next K1.
-template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false>
+template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
 __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
   constexpr int U = BKG_K3_ROWS;
-  if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
+  // XM: deferred X update, see kernels_mma.cuh k3_mma
+  const bool cur = *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) != 0;
+  const bool old = XM == 2 && *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xold) != 0;
+  if (!cur && !old) return;
   const bool fin = stopped(a.ctrl);  // uniform: nothing writes `done` during K3
+  const bool upd = cur && !fin;
+  const bool dox = XM != 1 || fin;
   extern __shared__ double sm[];
   double* lam = sm + S::RED;
   double* beta = lam + S::CS;
+  double* lamo = beta + S::CS;  // FastSmem reserves 3 coefficient blocks past RED
   for (int i = threadIdx.x; i < S::CS; i += kThreads) {
     lam[i] = a.coef[i];
     beta[i] = a.coef[2 * S::CS + i];
+    if (XM == 2) lamo[i] = a.coef[4 * S::CS + i];
   }
   __syncthreads();
   constexpr int NACC = P * CPT;
@@ -517,24 +528,28 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   const int goff = (GLOBAL ? 0 : col0 / P) * P * P;
   BKG_K3_COEF_PTR lg = lam + goff;
   BKG_K3_COEF_PTR bg = beta + goff;
+  BKG_K3_COEF_PTR og = lamo + goff;
+  double* Pout = XM == 0 ? a.P : a.Pn;
   const int64_t r1 = a.n;
   for (int64_t base = (int64_t)blockIdx.x * L::RPC * U; base < r1;
        base += (int64_t)gridDim.x * L::RPC * U) {
-    double pv[U][CPT], xv[U][CPT], rv[U][CPT], zv[U][CPT], dz[U];
+    double pv[U][CPT], ov[U][CPT], xv[U][CPT], rv[U][CPT], zv[U][CPT], dz[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t row = base + u * L::RPC + slot;
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) pv[u][j] = xv[u][j] = rv[u][j] = zv[u][j] = 0.0;
+      for (int j = 0; j < CPT; ++j) pv[u][j] = ov[u][j] = xv[u][j] = rv[u][j] = zv[u][j] = 0.0;
       dz[u] = 1.0;
       if (row < r1) {
-        ld_rw<CPT>(pv[u], a.P + row * K + col0);
-        ld_rw<CPT>(xv[u], a.X + row * K + col0);
-        if (!fin) ld_nc<CPT>(rv[u], a.R + row * K + col0);
+        if (cur) ld_rw<CPT>(pv[u], a.P + row * K + col0);
+        if constexpr (XM == 2)
+          if (old) ld_nc<CPT>(ov[u], a.Pold + row * K + col0);
+        if (dox) ld_rw<CPT>(xv[u], a.X + row * K + col0);
+        if (upd) ld_nc<CPT>(rv[u], a.R + row * K + col0);
         if constexpr (ZS)
-          if (!fin) ld_nc<CPT>(zv[u], a.zsrc + row * K + col0);
+          if (upd) ld_nc<CPT>(zv[u], a.zsrc + row * K + col0);
         if constexpr (JAC)
-          if (!fin) dz[u] = __ldg(a.zscale + row);
+          if (upd) dz[u] = __ldg(a.zscale + row);
       }
     }
 #pragma unroll
@@ -547,10 +562,13 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
 #pragma unroll
         for (int jj = 0; jj < CPT; ++jj) {
           const double ps = __shfl_sync(kFull, pv[u][jj], gbase + s);
+          double os = 0.0;
+          if constexpr (XM == 2) os = __shfl_sync(kFull, ov[u][jj], gbase + s);
           const int b = s * CPT + jj;
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
             const int e = b * P + (col0 + j) % P;
+            if constexpr (XM == 2) xv[u][j] = fma(os, og[e], xv[u][j]);
             xv[u][j] = fma(ps, lg[e], xv[u][j]);
             pn[j] = fma(ps, bg[e], pn[j]);
           }
@@ -558,10 +576,10 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
       }
       const int64_t row = base + u * L::RPC + slot;
       if (row < r1) {
-        st<CPT>(a.X + row * K + col0, xv[u]);
-        if (!fin) st<CPT>(a.P + row * K + col0, pn);
+        if (dox) st<CPT>(a.X + row * K + col0, xv[u]);
+        if (upd) st<CPT>(Pout + row * K + col0, pn);
       }
-      if (!fin) {
+      if (upd) {
 #pragma unroll
         for (int s = 0; s < L::GT; ++s) {
 #pragma unroll
@@ -578,8 +596,15 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
   }
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
-  if (!fin) gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
-  if (threadIdx.x == 0) a.ctrl->xpending = 0;  // every CTA has read it (we are last)
+  if (upd) gather_gram<K, P, CPT, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
+  if (XM == 1 && upd)
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.coef[4 * S::CS + i] = a.coef[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // every CTA has read the flags (we are last)
+    if (XM == 1) a.ctrl->xold = upd ? 1 : 0;
+    if (XM == 2) a.ctrl->xold = 0;
+    a.ctrl->xpending = 0;
+  }
 }
 
 // ------------------------------------------------------- K2 (ILU(0)) ---

@@ -248,18 +248,29 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
 }
 
 // ------------------------------------------------------------ K3 (DMMA) --
-// X += P lambda; unless stopped: P = R + P beta, rho_prev' = <<P', R>>.
-template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false>
+// X += P lambda; unless stopped: P' = Z + P beta (Z = R, D^-1 R or the ILU
+// sweeps' Z) into a.Pn, rho_prev' = <<P', R>>.
+// XM (deferred X update, the solver alternates 1 / 2 per iteration): 0 = X
+// every iteration; 1 = skip: X untouched (unless the solve ends here), lambda
+// saved to coef + 4 cs, ctrl->xold set, P' written to the other P buffer;
+// 2 = flush: X += Pold lambda_old + P lambda in one pass.  X is then read and
+// written every other iteration (K3 traffic 5nk -> 3nk / 6nk alternating).
+template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
-  if (*reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) == 0) return;
+  const bool cur = *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) != 0;
+  const bool old = XM == 2 && *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xold) != 0;
+  if (!cur && !old) return;
   const bool fin = stopped(a.ctrl);
+  const bool upd = cur && !fin;           // P' and the Gram
+  const bool dox = XM != 1 || fin;        // X written by this launch
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = warp % L::Q;
-  double lam[L::KC][L::NT], bet[L::KC][L::NT];
+  double lam[L::KC][L::NT], bet[L::KC][L::NT], lamo[L::KC][L::NT];
   load_bfrag<K, P, GLOBAL>(a.coef, g, 1.0, lam, lane);
   load_bfrag<K, P, GLOBAL>(a.coef + 2 * S::CS, g, 1.0, bet, lane);
+  if constexpr (XM == 2) load_bfrag<K, P, GLOBAL>(a.coef + 4 * S::CS, g, 1.0, lamo, lane);
   constexpr int NACC = L::NT * L::NT * 2;
   static_assert(L::TPR * NACC <= S::RED, "grid_reduce buffer");
   double acc[NACC];
@@ -269,86 +280,113 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::Q;
   const int col_a = g * L::PE + (lane & 3);
   const int col_c = g * L::PE + 2 * (lane & 3);
-  for (int64_t rb = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb < nrb;
-       rb += wstride) {
-    const int64_t row = rb * 8 + (lane >> 2);
-    const bool ok = row < a.n;
-    double pa[L::KC], xc[L::NT][2], pn[L::NT][2], zz[L::NT][2];
+  double* Pout = XM == 0 ? a.P : a.Pn;
+  // U row blocks per warp step, all loads issued before any DMMA: the skip
+  // launch (XM 1) streams only P and R, too few bytes in flight at one block
+  constexpr int U = (XM == 1 && P <= 8) ? 2 : 1;
+  for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
+       rb0 += U * wstride) {
+    double pa[U][L::KC], po[U][L::KC], xc[U][L::NT][2], pn[U][L::NT][2], zz[U][L::NT][2];
 #pragma unroll
-    for (int kc = 0; kc < L::KC; ++kc) pa[kc] = ok ? a.P[row * K + col_a + kc * 4] : 0.0;
-#pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) {
-      double t[2] = {0.0, 0.0}, r[2] = {0.0, 0.0}, zt[2] = {0.0, 0.0};
-      if (ok) {
-        ld_rw<2>(t, a.X + row * K + col_c + nt * 8);
-        if (!fin) ld_nc<2>(r, a.R + row * K + col_c + nt * 8);
-        if constexpr (ZS)
-          if (!fin) ld_nc<2>(zt, a.zsrc + row * K + col_c + nt * 8);
-      }
-      xc[nt][0] = t[0];
-      xc[nt][1] = t[1];
-      pn[nt][0] = r[0];
-      pn[nt][1] = r[1];
-      zz[nt][0] = zt[0];
-      zz[nt][1] = zt[1];
-    }
-    double tr[L::NT][2];
-    if (!fin) {
-#pragma unroll
-      for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tr[nt], lane);  // R, T layout
-      if constexpr (ZS) {  // P' = Z + P beta with Z from the ILU(0) sweeps
-#pragma unroll
-        for (int nt = 0; nt < L::NT; ++nt) {
-          pn[nt][0] = zz[nt][0];
-          pn[nt][1] = zz[nt][1];
-        }
-      }
-      if constexpr (JAC) {  // P' = Z + P beta with Z = D^-1 R (Jacobi)
-        const double dz = ok ? __ldg(a.zscale + row) : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < L::NT; ++nt) {
-          pn[nt][0] *= dz;
-          pn[nt][1] *= dz;
-        }
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt)
+    for (int u = 0; u < U; ++u) {
+      const int64_t rb = rb0 + u * wstride;
+      const int64_t row = rb * 8 + (lane >> 2);
+      const bool ok = rb < nrb && row < a.n;
 #pragma unroll
       for (int kc = 0; kc < L::KC; ++kc) {
-        dmma(xc[nt], pa[kc], lam[kc][nt]);
-        if (!fin) dmma(pn[nt], pa[kc], bet[kc][nt]);
+        pa[u][kc] = ok && cur ? a.P[row * K + col_a + kc * 4] : 0.0;
+        po[u][kc] = 0.0;
+        if constexpr (XM == 2) po[u][kc] = ok && old ? a.Pold[row * K + col_a + kc * 4] : 0.0;
       }
-    __syncwarp();
 #pragma unroll
-    for (int nt = 0; nt < L::NT; ++nt) {
-      if (ok) {
-        st<2>(a.X + row * K + col_c + nt * 8, xc[nt]);
-        if (!fin) st<2>(a.P + row * K + col_c + nt * 8, pn[nt]);
+      for (int nt = 0; nt < L::NT; ++nt) {
+        double t[2] = {0.0, 0.0}, r[2] = {0.0, 0.0}, zt[2] = {0.0, 0.0};
+        if (ok) {
+          if (dox) ld_rw<2>(t, a.X + row * K + col_c + nt * 8);
+          if (upd) ld_nc<2>(r, a.R + row * K + col_c + nt * 8);
+          if constexpr (ZS)
+            if (upd) ld_nc<2>(zt, a.zsrc + row * K + col_c + nt * 8);
+        }
+        xc[u][nt][0] = t[0];
+        xc[u][nt][1] = t[1];
+        pn[u][nt][0] = r[0];
+        pn[u][nt][1] = r[1];
+        zz[u][nt][0] = zt[0];
+        zz[u][nt][1] = zt[1];
       }
     }
-    if (!fin) {
-      double tp[L::NT][2];
 #pragma unroll
-      for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[nt], tp[nt], lane);
+    for (int u = 0; u < U; ++u) {
+      const int64_t rb = rb0 + u * wstride;
+      const int64_t row = rb * 8 + (lane >> 2);
+      const bool ok = rb < nrb && row < a.n;
+      double tr[L::NT][2];
+      if (upd) {
 #pragma unroll
-      for (int at = 0; at < L::NT; ++at)
+        for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[u][nt], tr[nt], lane);  // R, T layout
+        if constexpr (ZS) {  // P' = Z + P beta with Z from the ILU(0) sweeps
 #pragma unroll
-        for (int bt = 0; bt < L::NT; ++bt) {
-          double* gacc = acc + (at * L::NT + bt) * 2;
-          double d[2] = {gacc[0], gacc[1]};
-          dmma(d, tp[at][0], tr[bt][0]);
-          dmma(d, tp[at][1], tr[bt][1]);
-          gacc[0] = d[0];
-          gacc[1] = d[1];
+          for (int nt = 0; nt < L::NT; ++nt) {
+            pn[u][nt][0] = zz[u][nt][0];
+            pn[u][nt][1] = zz[u][nt][1];
+          }
         }
+        if constexpr (JAC) {  // P' = Z + P beta with Z = D^-1 R (Jacobi)
+          const double dz = ok ? __ldg(a.zscale + row) : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < L::NT; ++nt) {
+            pn[u][nt][0] *= dz;
+            pn[u][nt][1] *= dz;
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < L::KC; ++kc) {
+          if constexpr (XM == 2)
+            if (old) dmma(xc[u][nt], po[u][kc], lamo[kc][nt]);
+          if (dox && cur) dmma(xc[u][nt], pa[u][kc], lam[kc][nt]);
+          if (upd) dmma(pn[u][nt], pa[u][kc], bet[kc][nt]);
+        }
+      __syncwarp();
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) {
+        if (ok) {
+          if (dox) st<2>(a.X + row * K + col_c + nt * 8, xc[u][nt]);
+          if (upd) st<2>(Pout + row * K + col_c + nt * 8, pn[u][nt]);
+        }
+      }
+      if (upd) {
+        double tp[L::NT][2];
+#pragma unroll
+        for (int nt = 0; nt < L::NT; ++nt) d_to_t(pn[u][nt], tp[nt], lane);
+#pragma unroll
+        for (int at = 0; at < L::NT; ++at)
+#pragma unroll
+          for (int bt = 0; bt < L::NT; ++bt) {
+            double* gacc = acc + (at * L::NT + bt) * 2;
+            double d[2] = {gacc[0], gacc[1]};
+            dmma(d, tp[at][0], tr[bt][0]);
+            dmma(d, tp[at][1], tr[bt][1]);
+            gacc[0] = d[0];
+            gacc[1] = d[1];
+          }
+      }
     }
   }
   extern __shared__ double sm[];
   double* red = sm;
   if (!grid_reduce<L::TPR, NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group)) return;
-  if (!fin) gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
-  if (threadIdx.x == 0) a.ctrl->xpending = 0;
+  if (upd) gather_gram_mma<K, P, GLOBAL, NACC>(red, 0, (a.dist ? a.red1 : a.coef) + S::CS);
+  if (XM == 1 && upd)
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.coef[4 * S::CS + i] = a.coef[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (XM == 1) a.ctrl->xold = upd ? 1 : 0;
+    if (XM == 2) a.ctrl->xold = 0;
+    a.ctrl->xpending = 0;
+  }
 }
 
 }  // namespace bkg
