@@ -1377,7 +1377,13 @@ int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
       out[0] = 2.0 * nk8 + csr;  // K1: read P (once, neighbours via L1/L2); write Q; CSR
       const double jac = s->precond == BKG_PRECOND_JACOBI ? 8.0 * (double)s->n : 0.0;
       out[1] = 3.0 * nk8 + jac;  // K2: read Q, R; write R (+ D^-1 for Jacobi)
-      out[2] = 5.0 * nk8 + jac;  // K3: read P, X, R; write P, X (+ D^-1)
+      // K3: read P, X, R; write P, X (+ D^-1); deferred X: skip launches read
+      // P, R and write P (3nk), flush launches also read P_old and read/write
+      // X (6nk) -- 4.5nk per launch on average
+      out[2] = (BKG_DEFER_X ? 4.5 : 5.0) * nk8 + jac;
+      if (s->precond == BKG_PRECOND_ILU0) {  // + Z read in K3; K2a has no Gram
+        out[2] += nk8;
+      }
     } else {  // exact mode: model of the unfused kernel sequence
       out[0] = 2.0 * nk8 + csr + 4.0 * nk8;  // spmm + alpha/rho_prev chains
       out[1] = 8.0 * nk8;                    // 2 baxpy + copy + rho/norm chains

@@ -499,8 +499,10 @@ template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false,
 __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
-  constexpr int U = BKG_K3_ROWS;
-  // XM: deferred X update, see kernels_mma.cuh k3_mma
+  // XM: deferred X update, see kernels_mma.cuh k3_mma; the skip launch
+  // streams only P and R, so it takes two rows per thread step where the
+  // per-row coefficient work is small (P * CPT <= 2; measured on B200)
+  constexpr int U = (XM == 1 && P * CPT <= 2) ? 2 : BKG_K3_ROWS;
   const bool cur = *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) != 0;
   const bool old = XM == 2 && *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xold) != 0;
   if (!cur && !old) return;

@@ -35,11 +35,13 @@ def main(rep, md, tj):
     traffic = {}
     for r in raw[2:]:
         rid = r[col["ID"]]
-        rd = float(r[col["dram__bytes_read.sum"]].replace(",", ""))
-        wr = float(r[col["dram__bytes_write.sum"]].replace(",", ""))
-        unit_r = raw[1][col["dram__bytes_read.sum"]]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-        per.setdefault(rid, {})["dram_bytes"] = (rd + wr) * scale
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def nbytes(metric):  # each metric carries its own unit
+            v = float(r[col[metric]].replace(",", ""))
+            return v * scale.get(raw[1][col[metric]], 1)
+        per.setdefault(rid, {})["dram_bytes"] = (nbytes("dram__bytes_read.sum") +
+                                                 nbytes("dram__bytes_write.sum"))
         stalls = {}
         for n, i in col.items():
             if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("_not_issued"):
@@ -60,7 +62,9 @@ def main(rep, md, tj):
                      f" | {p.get('dram_bytes', 0) / 1e6:.1f} MB | {p.get('stalls', '')} |")
         key = ("K1_spmm_gram" if "k1" in name else "K2_update_gram" if "k2" in name
                else "K3_update_p" if "k3" in name else name)
-        traffic[key] = p.get("dram_bytes")
+        traffic.setdefault(key, []).append(p.get("dram_bytes"))
+    # per launch; K3 alternates skip / flush launches (deferred X): the mean
+    traffic = {k: sum(v) / len(v) for k, v in traffic.items() if all(x is not None for x in v)}
     open(md, "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(tj, "w"), indent=1)
     print("\n".join(lines))
