@@ -127,13 +127,22 @@ __device__ void gather_norms_mma(const double* red, int off, double* norms, bool
 // and K3 (two coefficient blocks) at 2.
 // K2 with P <= 8 processes two row blocks per warp step (3 CTAs/SM): C2 K2
 // 0.281 -> 0.265 ms; at P = 16 the doubled tile costs more than it hides.
+#ifndef BKG_K2_U8
+#define BKG_K2_U8 2
+#endif
+#ifndef BKG_K2_MINB8
+#define BKG_K2_MINB8 3
+#endif
+#ifndef BKG_K3_MINB8
+#define BKG_K3_MINB8 4
+#endif
 template <int P>
 constexpr int k2_unroll() {
-  return P <= 8 ? 2 : 1;
+  return P <= 8 ? BKG_K2_U8 : 1;
 }
 template <int P, int KERNEL>
 constexpr int mma_minb() {
-  return P <= 8 ? (KERNEL == 2 ? 3 : 4) : (KERNEL == 2 ? 3 : 2);
+  return P <= 8 ? (KERNEL == 2 ? BKG_K2_MINB8 : BKG_K3_MINB8) : (KERNEL == 2 ? 3 : 2);
 }
 template <int K, int P, bool GLOBAL, bool JAC = false>
 __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs a) {
