@@ -142,6 +142,11 @@ __global__ void k_ilu_bwd_level(const Ctrl* ctrl, const int32_t* __restrict__ ro
 #ifndef BKG_ILU_ELL
 #define BKG_ILU_ELL 1
 #endif
+// Lanes per segment for 16 < k <= 32 in the ELL sweep (16 would run two
+// segments per warp with two columns per lane: C2 apply 2.46 -> 3.56 ms)
+#ifndef BKG_ILU_W32
+#define BKG_ILU_W32 32
+#endif
 // Longest sync-free sweep segment (rows per ticket).
 #ifndef BKG_ILU_SEG
 #define BKG_ILU_SEG 256
@@ -249,11 +254,13 @@ __global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const C
   if (stopped(ctrl)) return;
   // k <= 16: the warp splits into 32 / W lane groups of W = 8 or 16 lanes,
   // each sweeping its own segment (more segments in flight per register)
-  const int W = k <= 8 ? 8 : (k <= 16 ? 16 : 32);
+  // lane groups of W lanes, two columns per lane (lane, lane + W) when k > W:
+  // k <= 8: W = 8, k <= 16: 16, k <= 64: 32
+  const int W = k <= 8 ? 8 : (k <= 16 ? 16 : (k <= 32 ? BKG_ILU_W32 : 32));
   const int wl = threadIdx.x & 31, g = wl / W;
   const int lane = wl % W;  // column index within the group
   const unsigned gmask = W == 32 ? 0xffffffffu : (((1u << W) - 1u) << (g * W));
-  const bool c0 = lane < k, c1 = lane + 32 < k;
+  const bool c0 = lane < k, c1 = lane + W < k;
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1ull);
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const C
       vv[u] = evals[first * D + u];
     }
     if (c0) s0 = src[first * k + lane];
-    if (c1) s1 = src[first * k + lane + 32];
+    if (c1) s1 = src[first * k + lane + W];
     double p0 = 0.0, p1 = 0.0;
     for (int i = 0; i < cnt; ++i) {
       const int64_t row = FWD ? first + i : first - i;
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const C
           nv[u] = evals[nr * D + u];
         }
         if (c0) n0 = src[nr * k + lane];
-        if (c1) n1 = src[nr * k + lane + 32];
+        if (c1) n1 = src[nr * k + lane + W];
       }
       double a0 = s0, a1 = s1;
 #pragma unroll
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const C
           x1 = p1;
         } else {
           if (c0) x0 = ld_ready(out + (int64_t)cc[u] * k + lane);
-          if (c1) x1 = ld_ready(out + (int64_t)cc[u] * k + lane + 32);
+          if (c1) x1 = ld_ready(out + (int64_t)cc[u] * k + lane + W);
         }
         a0 = __dsub_rn(a0, __dmul_rn(vv[u], x0));
         a1 = __dsub_rn(a1, __dmul_rn(vv[u], x1));
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(256, (D <= 8 ? 4 : 3)) k_ilu_sweep_ell(const C
         a1 = __dmul_rn(a1, d);
       }
       if (c0) out[row * k + lane] = not_sentinel(a0);
-      if (c1) out[row * k + lane + 32] = not_sentinel(a1);
+      if (c1) out[row * k + lane + W] = not_sentinel(a1);
       p0 = a0;
       p1 = a1;
 #pragma unroll
@@ -551,6 +558,11 @@ inline void precond_ready(bkg_ctx* c, bkg_matrix* a, int kind) {
   if (kind == BKG_PRECOND_ILU0) ilu_ready(c, a);
 }
 
+// Lanes per segment for 16 < k <= 32 in the ELL sweep (16 would run two
+// segments per warp with two columns per lane: C2 apply 2.46 -> 3.56 ms)
+#ifndef BKG_ILU_W32
+#define BKG_ILU_W32 32
+#endif
 // Longest sync-free sweep segment (rows per ticket).
 #ifndef BKG_ILU_WARPS
 #define BKG_ILU_WARPS 0  // cap on concurrent sweep warps (0: one full wave)
