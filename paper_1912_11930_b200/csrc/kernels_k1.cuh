@@ -3,20 +3,23 @@
 // (kernels.hpp:231-240).
 //
 // Row layout: a lane owns CPL = 4 consecutive columns of one row and reads
-// each CSR operand row segment as one 32-byte LDG.256, so LPR = W / 4 lanes
-// cover the warp's W columns of a row and a warp tile is RPW = 32 / LPR rows.  Compared with the 16-byte k1_tile this halves the number of lanes
-// that replicate each row's CSR stream (the replicated (value, column) loads
-// were ~40% of K1's L1->register traffic on B200, ncu) and halves the gather
-// instructions.  The Gram P^T Q over the tile is FP64 DMMA (m8n8k4, k = 4 rows
-// per MMA): the tile's P and Q rows go through a per-warp shared-memory
-// scratch into the T (operand) layout instead of warp shuffles.
-// Rows of a tile past n contribute zeros.
+// each operand row segment as one 32-byte LDG.256, so LPR = W / 4 lanes cover
+// the warp's W columns of a row and a warp tile is RPW = 32 / LPR rows.
+// Compared with the 16-byte k1_tile this halves the number of lanes that
+// replicate each row's (value, column) stream (~40% of K1's L1->register
+// traffic on B200, ncu) and halves the gather instructions.  The matrix is
+// read from its sliced-ELL copy (common.cuh SellCsr, slice height = RPW).
+// The Gram P^T Q over the tile is FP64 DMMA (m8n8k4, k = 4 rows per MMA): the
+// tile's P and Q rows go through a per-warp shared-memory scratch into the T
+// (operand) layout.  Rows of a tile past n contribute zeros.
 #pragma once
 
 #include "kernels_mma.cuh"
 
 namespace bkg {
 
+// Cache operator of the operand gathers (tools/kernel_sweep.py variants): 0
+// .nc (default, best), 1 .cg, 2 .nc.L1::no_allocate, 3 .nc.L1::evict_last.
 #ifndef BKG_K1W_LD
 #define BKG_K1W_LD 0
 #endif
