@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   double* Pout = XM == 0 ? a.P : a.Pn;
   // U row blocks per warp step, all loads issued before any DMMA: the skip
   // launch (XM 1) streams only P and R, too few bytes in flight at one block
-  constexpr int U = (XM == 1 && P <= 8) ? 2 : 1;
+  constexpr int U = (XM == 1 && (P <= 8 || K == 64)) ? 2 : 1;  // C4 p = 16: slower
   for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
        rb0 += U * wstride) {
     double pa[U][L::KC], po[U][L::KC], xc[U][L::NT][2], pn[U][L::NT][2], zz[U][L::NT][2];
