@@ -116,3 +116,36 @@ def _reversal_floor(port, csr, b, p, glob, hist):
                          np.ascontiguousarray(b[perm]), p, glob, tol=1e-8, max_iter=500,
                          record_history=True)
     return _drift(rev.history, hist)
+
+
+@pytest.mark.parametrize("k,p,glob", [(8, 4, False), (16, 16, False), (32, 8, False),
+                                      (64, 4, True)])
+@pytest.mark.parametrize("hub", [60, 8])
+def test_ilu_irregular_exact_bitwise_and_fast_bars(port, k, p, glob, hub):
+    """ILU(0) on an irregular pattern: hub = 60 puts more than 16 entries in a
+    triangle row (CSR sweeps), hub = 8 keeps every row ELL-sized; the row
+    segments of the sync-free sweeps are mostly single rows here (random
+    pattern, few previous-row chains).  Exact mode must be bitwise the
+    reference; fast mode meets X 1e-8 and the iteration bars."""
+    n = 1499
+    csr = irregular(n, seed=17 + k + p + hub, hub=hub)
+    a = bk.SparseMatrix(n, *csr)
+    b = bk.normal_block_rhs(n, k, 7)
+    cfg = bk.SubalgebraConfig(k, p, "global" if glob else "hybrid")
+    opts = bk.SolveOptions(tol=1e-8, max_iter=300, record_history=True)
+    ref = port.bcg_solve(csr, b, p, glob and p != k, tol=1e-8, max_iter=300,
+                         record_history=True, precond="ilu0")
+    for mode in ("exact", "fast"):
+        ctx = bk.Context(0, mode)
+        res = bk.bcg_solve(a, b, bk.ilu0_factor(a, ctx), cfg, opts, ctx=ctx)
+        r = res.report
+        assert r.converged and ref.report.converged
+        if mode == "exact":
+            assert r.iterations == ref.report.iterations
+            assert np.array(r.defect_history).tobytes() == ref.history.tobytes()
+            assert res.x.tobytes() == ref.x.tobytes()
+        else:
+            xr = np.linalg.norm(res.x - ref.x, axis=0) / np.linalg.norm(ref.x, axis=0)
+            assert np.max(xr) <= 1e-8, xr
+            assert abs(r.iterations - ref.report.iterations) <= max(1, int(0.05 * ref.report.iterations))
+        ctx.close()
