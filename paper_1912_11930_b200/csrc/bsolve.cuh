@@ -32,7 +32,7 @@ __host__ __device__ inline int bsolve_ws_doubles(int p, int nthreads) {
   const int par = bsolve_par(p, nthreads);
   const int pp = p * p;
   const int ints = par * p + 2 * par + 1;
-  return par * (2 * pp + 1) + (ints + 1) / 2 + 1;
+  return par * (2 * pp + 1 + p) + (ints + 1) / 2 + 1;
 }
 
 // Returns (to every thread) the smallest failing block index, or -1.
@@ -54,7 +54,11 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
   double* lu_all = ws;
   double* res_all = ws + par * pp;
   double* maxn_all = ws + 2 * par * pp;
-  int* perm_all = reinterpret_cast<int*>(ws + par * (2 * pp + 1));
+  // 1 / pivot of every elimination step, computed once by the pivot thread
+  // (the same __ddiv_rn the reference applies to the same value, so bits are
+  // unchanged) and reused by the elimination and the back substitution
+  double* inv_all = maxn_all + par;
+  int* perm_all = reinterpret_cast<int*>(ws + par * (2 * pp + 1 + p));
   int* piv_all = perm_all + par * p;
   int* brk_all = piv_all + par;
   int* bad_s = brk_all + par;
@@ -67,6 +71,7 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
     const bool live = in_grp && blk < nblk;
     double* lu = lu_all + gi * pp;
     double* res = res_all + gi * pp;
+    double* invp = inv_all + gi * p;
     int* perm = perm_all + gi * p;
     if (live) {
       for (int el = gt; el < pp; el += grp) lu[el] = gamma[(size_t)blk * pp + el];
@@ -101,6 +106,8 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
         }
         if (pivot < tiny || max_norm == 0.0) brk_all[gi] = 1;
         piv_all[gi] = pivot_row;
+        // lu[col][col] after the row swap
+        invp[col] = __ddiv_rn(1.0, lu[pivot_row * p + col]);
       }
       __syncthreads();
       const bool go = live && !brk_all[gi];
@@ -124,7 +131,7 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
       // elimination (kernels.hpp:200-205).  Phase 1 updates the trailing
       // block (reads lu[r][col], untouched here); phase 2 stores f.
       if (go) {
-        const double inv = __ddiv_rn(1.0, lu[col * p + col]);
+        const double inv = invp[col];
         for (int el = gt; el < pp; el += grp) {
           const int r = el / p, c = el - r * p;
           if (r > col && c > col) {
@@ -135,7 +142,7 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
       }
       __syncthreads();
       if (go) {
-        const double inv = __ddiv_rn(1.0, lu[col * p + col]);
+        const double inv = invp[col];
         for (int r = col + 1 + gt; r < p; r += grp) lu[r * p + col] = __dmul_rn(lu[r * p + col], inv);
       }
       __syncthreads();
@@ -154,8 +161,7 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
           double acc = res[r * p + c];
           for (int j = r + 1; j < p; ++j)
             acc = __dsub_rn(acc, __dmul_rn(lu[r * p + j], res[j * p + c]));
-          const double inv = __ddiv_rn(1.0, lu[r * p + r]);
-          res[r * p + c] = __dmul_rn(acc, inv);
+          res[r * p + c] = __dmul_rn(acc, invp[r]);  // = __ddiv_rn(1.0, lu[r][r])
         }
       }
     }
