@@ -326,9 +326,88 @@ __global__ void k_sell_fill(int64_t n, int R, const int64_t* __restrict__ rowptr
   }
 }
 
+// Line variant (SellCsr::run > 0): row of (slice s, position i) and the
+// number of a row's entries in columns r - 1, r, r + 1 (CSR columns ascend).
+__device__ __forceinline__ int64_t line_row(int64_t s, int i, int R, int run) {
+  return (s / run) * ((int64_t)R * run) + (int64_t)i * run + s % run;
+}
+__device__ __forceinline__ int tri_count(int64_t r, const int64_t* rowptr, const int32_t* cols) {
+  int m = 0;
+  for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+    const int64_t d = (int64_t)cols[e] - r;
+    m += (d >= -1 && d <= 1);
+  }
+  return m;
+}
+
+__global__ void k_sell_width_line(int64_t ns, int64_t n, int R, int run,
+                                  const int64_t* __restrict__ rowptr,
+                                  const int32_t* __restrict__ cols, int64_t* __restrict__ sptr) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < ns;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t w = 0;
+    for (int i = 0; i < R; ++i) {
+      const int64_t r = line_row(s, i, R, run);
+      if (r < n) w = max(w, rowptr[r + 1] - rowptr[r] - tri_count(r, rowptr, cols));
+    }
+    sptr[s + 1] = w * R;
+    if (s == 0) sptr[0] = 0;
+  }
+}
+
+// One thread per (slice, position): the row's entries outside columns
+// r - 1 .. r + 1 fill the slots in CSR order, those three go to tri.
+__global__ void k_sell_fill_line(int64_t ns, int64_t n, int R, int run,
+                                 const int64_t* __restrict__ rowptr,
+                                 const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                 const int64_t* __restrict__ sptr, int32_t* __restrict__ scols,
+                                 double* __restrict__ svals, double* __restrict__ tri) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ns * R;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = idx / R;
+    const int i = (int)(idx % R);
+    const int64_t r = line_row(s, i, R, run);
+    const int64_t b = sptr[s], w = (sptr[s + 1] - b) / R;
+    double t3[3] = {0.0, 0.0, 0.0};
+    int64_t u = 0;
+    if (r < n) {
+      for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+        const int64_t d = (int64_t)cols[e] - r;
+        if (d >= -1 && d <= 1) {
+          t3[d + 1] = vals[e];
+        } else {
+          svals[b + u * R + i] = vals[e];
+          scols[b + u * R + i] = cols[e];
+          ++u;
+        }
+      }
+    }
+    for (; u < w; ++u) {
+      svals[b + u * R + i] = 0.0;
+      scols[b + u * R + i] = kNoCol;
+    }
+    double* o = tri + idx * 4;
+    o[0] = t3[0];
+    o[1] = t3[1];
+    o[2] = t3[2];
+    o[3] = 0.0;
+  }
+}
+
+// Entries of A in columns r - 1, r, r + 1 (the line variant's window terms).
+__global__ void k_count_tri(int64_t n, const int64_t* __restrict__ rowptr,
+                            const int32_t* __restrict__ cols, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    m += tri_count(r, rowptr, cols);
+  if (m) atomicAdd(out, m);
+}
+
 void sell_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
-                const double* vals, int R, SellCsr& out, SellCsr* spare) {
-  const int64_t ns = std::max<int64_t>(1, (n + R - 1) / R);
+                const double* vals, int R, SellCsr& out, SellCsr* spare, int run) {
+  const int64_t ns = run > 0 ? std::max<int64_t>(1, (n + (int64_t)R * run - 1) / ((int64_t)R * run)) * run
+                             : std::max<int64_t>(1, (n + R - 1) / R);
   if (spare && spare->sptr.count >= (size_t)ns + 1 && out.sptr.count < (size_t)ns + 1)
     out.sptr = std::move(spare->sptr);
   out.sptr.ensure((size_t)ns + 1);
@@ -336,8 +415,15 @@ void sell_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* col
     int64_t nn = n;
     int rr = R;
     int64_t* sp = out.sptr.ptr;
-    void* args[] = {&nn, &rr, &rowptr, &sp};
-    launch(c, (const void*)&k_sell_width, elem_grid(c, ns), 256, 0, args);
+    if (run > 0) {
+      int64_t nss = ns;
+      int ru = run;
+      void* args[] = {&nss, &nn, &rr, &ru, &rowptr, &cols, &sp};
+      launch(c, (const void*)&k_sell_width_line, elem_grid(c, ns), 256, 0, args);
+    } else {
+      void* args[] = {&nn, &rr, &rowptr, &sp};
+      launch(c, (const void*)&k_sell_width, elem_grid(c, ns), 256, 0, args);
+    }
   }
   size_t tmp_bytes = 0;
   BKG_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, out.sptr.ptr + 1,
@@ -361,9 +447,19 @@ void sell_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* col
     const int64_t* sp = out.sptr.ptr;
     int32_t* sc = out.cols.ptr;
     double* sv = out.vals.ptr;
-    void* args[] = {&nn, &rr, &rowptr, &cols, &vals, &sp, &sc, &sv};
-    launch(c, (const void*)&k_sell_fill, elem_grid(c, ns * 32), 256, 0, args);
+    if (run > 0) {
+      out.tri.ensure((size_t)ns * R * 4);
+      int64_t nss = ns;
+      int ru = run;
+      double* tr = out.tri.ptr;
+      void* args[] = {&nss, &nn, &rr, &ru, &rowptr, &cols, &vals, &sp, &sc, &sv, &tr};
+      launch(c, (const void*)&k_sell_fill_line, elem_grid(c, ns * R), 256, 0, args);
+    } else {
+      void* args[] = {&nn, &rr, &rowptr, &cols, &vals, &sp, &sc, &sv};
+      launch(c, (const void*)&k_sell_fill, elem_grid(c, ns * 32), 256, 0, args);
+    }
   }
+  out.run = run;
   out.rows = R;
   out.n = n;
 }
@@ -409,6 +505,42 @@ __global__ void k_ilu_finish(Ctrl* ctrl, int nblk, int p, int k, double* coef, i
   finish_iteration(ctrl, norms, limits, hist, ring, k);
 }
 
+// K1 choice per matrix: k1_line where it measured faster for this (K, P)
+// (ft.line_auto), enough of A sits in columns r - 1 .. r + 1 (stencils
+// numbered along x: 3/7 of a 7-point row, 3/5 of a 5-point one; 3/27 on a
+// 27-point row, where the window saves too little) and the system is large
+// enough for every resident warp to get >= 2 super tiles of runs.
+// BKG_K1_LINE=0/1 forces it off/on (sweeps, tests).
+bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
+  if (!ft.k1_line || A->n == 0) return false;
+  const char* env = std::getenv("BKG_K1_LINE");
+  if (env && env[0] == '0') return false;
+  const bool forced = env && env[0] == '1';
+  if (A->tri_nnz < 0) {
+    DevBuf<unsigned long long> cnt(1);
+    BKG_CUDA_CHECK(cudaMemsetAsync(cnt.ptr, 0, sizeof(unsigned long long), c->stream));
+    int64_t nn = (int64_t)A->n;
+    const int64_t* rp = A->rowptr.ptr;
+    const int32_t* cl = A->cols.ptr;
+    unsigned long long* o = cnt.ptr;
+    void* args[] = {&nn, &rp, &cl, &o};
+    launch(c, (const void*)&k_count_tri, elem_grid(c, nn), 256, 0, args);
+    unsigned long long h = 0;
+    d2h(c, &h, cnt.ptr, 1);
+    sync(c);
+    A->tri_nnz = (int64_t)h;
+  }
+  if (forced) return true;
+  if (!ft.line_auto) return false;
+  if ((double)A->tri_nnz < 0.2 * (double)A->nnz) return false;
+  int nb = 0;
+  allow_smem(ft.k1_line, ft.smem_k1);
+  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ft.k1_line, kThreads,
+                                                               ft.smem_k1));
+  const int64_t need = ((int64_t)A->n + ft.rpc_k1_line - 1) / ft.rpc_k1_line;
+  return need >= 2 * (int64_t)std::max(nb, 1) * c->sm_count;
+}
+
 // =========================================================== solver =====
 struct bkg_solver {
   bkg_ctx* ctx = nullptr;
@@ -420,6 +552,7 @@ struct bkg_solver {
   bool fast = false;
   FastTable ft;
   int g1 = 1, g2 = 1, g3 = 1;
+  int k1_run = 0;  // K1 = k1_line over the line-variant sliced ELL (run length)
   const void* k2fn = nullptr;  // ft.k2 / ft.k2_jac (Jacobi folded into the loop)
   const void* k3fn = nullptr;
   int g2i = 1, gg = 1;          // ILU(0) loop: k2_ilu and Gram grids
@@ -510,6 +643,11 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
+      if (use_line(c, A, ft)) {
+        ft.k1 = ft.k1_line;
+        ft.rpc_k1 = ft.rpc_k1_line;
+        k1_run = ft.line_run;
+      }
       g1 = occupancy_grid(c, ft.k1, ft.smem_k1, n, ft.rpc_k1);
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
@@ -556,12 +694,13 @@ struct bkg_solver {
     if (fast && ft.sell_rows) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
       // capture: launch_chunk calls iter_args before capturing)
-      if (A->sell.rows != ft.sell_rows || A->sell.n != n)
+      if (A->sell.rows != ft.sell_rows || A->sell.n != n || A->sell.run != k1_run)
         sell_build(ctx, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, ft.sell_rows, A->sell,
-                   &ctx->spare_sell);
+                   &ctx->spare_sell, k1_run);
       a.sptr = A->sell.sptr.ptr;
       a.scols = A->sell.cols.ptr;
       a.svals = A->sell.vals.ptr;
+      a.stri = k1_run ? A->sell.tri.ptr : nullptr;
     }
     return a;
   }

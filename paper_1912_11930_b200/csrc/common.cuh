@@ -119,9 +119,18 @@ __device__ __forceinline__ bool stopped(const Ctrl* c) {
 // (entry (slot u, row i) of slice s at sptr[s] + u * R + i; padding: value 0,
 // column kNoCol), so the R rows of a K1 warp tile read each slot's values and
 // columns as one contiguous segment.  Built on device from the CSR.
+//
+// Line variant (run > 0, k1_line): slice s holds rows
+// (s / run) * R * run + i * run + s % run, i < R -- each of the R rows of a
+// warp step starts its own run of `run` consecutive rows -- and the entries in
+// columns r - 1, r, r + 1 of row r are taken out of the slots into
+// tri[(s * R + i) * 4 + {0, 1, 2}] (0 where absent), because k1_line keeps
+// P[r - 1], P[r], P[r + 1] of its run in registers.
 struct SellCsr {
   int rows = 0;  // slice height R (0: not built)
+  int run = 0;   // line variant: rows per run (0: slices of R consecutive rows)
   int64_t n = 0;
+  DevBuf<double> tri;    // line variant: 4 doubles per slice row
   DevBuf<int64_t> sptr;  // nslices + 1 entry offsets
   DevBuf<int32_t> cols;
   DevBuf<double> vals;
@@ -163,6 +172,7 @@ struct bkg_matrix {
   bkg::DevBuf<double> vals;
   // sliced-ELL copy for the fused K1 (built lazily by the first fast solve)
   mutable bkg::SellCsr sell;
+  mutable int64_t tri_nnz = -1;  // entries in columns r - 1 .. r + 1 (counted lazily)
   // preconditioner data (built lazily on device)
   bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)
   bkg::DevBuf<double> lu;        // ILU(0) factors on A's pattern

@@ -36,6 +36,16 @@ constexpr int k1w_chunk() {
 }
 #endif
 
+// k1_line (line-variant sliced ELL, kernels_k1.cuh): rows per run and CSR
+// chunk (slots left after the r-1, r, r+1 entries are taken out: 4 on a
+// 7-point stencil, 2 on a 5-point one).
+#ifndef BKG_K1L_RUN
+#define BKG_K1L_RUN 32
+#endif
+#ifndef BKG_K1L_CH
+#define BKG_K1L_CH 4
+#endif
+
 struct FastTable {
   const void* k1 = nullptr;
   const void* k2 = nullptr;
@@ -63,6 +73,11 @@ struct FastTable {
   int rpc_k3 = 1;
   int rpc_k1 = 1;     // rows per CTA pass of K1
   int sell_rows = 0;  // K1 reads a sliced-ELL copy with this slice height (0: CSR)
+  // k1_line alternative (picked per matrix by the solver, api.cu use_line)
+  const void* k1_line = nullptr;
+  int rpc_k1_line = 1;  // rows per CTA pass (RPW x run per warp group)
+  int line_run = 0;
+  bool line_auto = false;  // the solver may pick it (measured winner for this (K, P))
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -88,6 +103,12 @@ void fill_table(FastTable* t) {
     t->smem_k1 = k1_wide_smem<K, P, W, 4, G>();
     t->sell_rows = WL::RPW;
     if (WL::RED > t->e_iter) t->e_iter = WL::RED;
+    t->k1_line = (const void*)&k1_line<K, P, W, 4, BKG_K1L_CH, BKG_K1L_RUN, G>;
+    t->rpc_k1_line = t->rpc_k1 * BKG_K1L_RUN;
+    t->line_run = BKG_K1L_RUN;
+    // B200 sweeps: k1_line wins only at K = 64, P >= 8 (C5
+    // 7.42 -> 7.16 ms); at K <= 32 and K = 64, P < 8 it is 2-19% slower.
+    t->line_auto = K == 64 && P >= 8;
   } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;

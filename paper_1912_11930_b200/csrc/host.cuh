@@ -25,7 +25,7 @@ void dev_gram(bkg_ctx* c, int64_t n, int k, int p, bool global, const double* x,
 // Build (or rebuild) `out` as the sliced-ELL copy of a device CSR with slice
 // height R; buffers are reused when large enough (spare: donor buffers).
 void sell_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
-                const double* vals, int R, SellCsr& out, SellCsr* spare = nullptr);
+                const double* vals, int R, SellCsr& out, SellCsr* spare = nullptr, int run = 0);
 void dev_spmm(bkg_ctx* c, const bkg_matrix* A, int k, const double* x, double* y, const Ctrl* ctrl,
               bool force_exact);
 

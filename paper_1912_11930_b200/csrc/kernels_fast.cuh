@@ -193,6 +193,7 @@ struct IterArgs {
   const int64_t* sptr;
   const int32_t* scols;
   const double* svals;
+  const double* stri;  // line variant (k1_line): tri-diagonal entries per slice row
   // Deferred X update (K3 template XM): K3 writes P' to Pn; in a flush
   // launch X += Pold lambda_old + P lambda (lambda_old at coef + 4 cs).
   double* Pn;

@@ -298,6 +298,198 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_wide(IterArgs a) {
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 
+// k1_line — k1_wide over the line variant of the sliced-ELL copy (common.cuh
+// SellCsr, run = LR): lane group rr of a warp walks LR consecutive rows
+// r = base + t, so P[r - 1], P[r], P[r + 1] stay in registers as a sliding
+// window -- one operand load per row (P[r + 1]) replaces the gathers of the
+// entries in columns r - 1, r, r + 1 AND the separate diagonal load of the
+// Gram (P[r] is the window centre).  On a 7-point stencil that is 5 instead of
+// 8 operand row loads per row (5-point: 3 instead of 6).  Same epilogue,
+// Gram, grid reduction and lambda solve as k1_wide; the products of a row are
+// summed as slots first, then the three window terms (fast-mode order).
+template <int K, int P, int W, int CPL, int CH, int LR, bool GLOBAL>
+__global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
+  using L = WideLayout<K, P, W, CPL>;
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  if (stopped(a.ctrl)) return;
+  constexpr int LPR = L::LPR, RPW = L::RPW, SS = L::SS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rr = lane / LPR, cl = lane % LPR;
+  const int col = (warp % L::QW) * W + cl * CPL;
+  const double* Pc = a.P + col;
+  extern __shared__ double sm[];
+  double* sp = sm + warp * L::SCR;
+  double* sq = sp + RPW * SS;
+  double acc[L::NACC];
+#pragma unroll
+  for (int e = 0; e < L::NACC; ++e) acc[e] = 0.0;
+  const int64_t nsup = (a.n + RPW * LR - 1) / (RPW * LR);
+  const int64_t nslice = nsup * LR;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32) / L::QW;
+  int64_t sup = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::QW;
+
+  auto extent = [&](int64_t s, int64_t& b, int& w) {
+    b = 0;
+    w = 0;
+    if (s < nslice) {
+      b = __ldg(a.sptr + s);
+      w = (int)((__ldg(a.sptr + s + 1) - b) / RPW);
+    }
+  };
+  auto load_chunk = [&](int64_t b, int off, int w, double (&v)[CH], int (&c)[CH]) {
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const bool in = off + u < w;
+      const int64_t e = b + (int64_t)(off + u) * RPW + rr;
+      v[u] = in ? __ldg(a.svals + e) : 0.0;
+      c[u] = in ? __ldg(a.scols + e) : kNoCol;
+    }
+  };
+  auto load_tri = [&](int64_t s, double (&d)[4]) {
+    if (s < nslice) {
+      ldg4(d, a.stri + (s * RPW + rr) * 4);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) d[t] = 0.0;
+    }
+  };
+  auto gather_fma = [&](const double (&v)[CH], const int (&c)[CH], double (&q)[CPL]) {
+    double x[CH][CPL];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      if (c[u] != kNoCol) {
+        ldg4(x[u], Pc + (int64_t)c[u] * K);
+      } else {
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) x[u][t] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) q[t] = fma(v[u], x[u][t], q[t]);
+  };
+  auto load_row = [&](int64_t r, double (&d)[CPL]) {
+    if (r >= 0 && r < a.n) {
+      ldg4(d, Pc + r * K);
+    } else {
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) d[t] = 0.0;
+    }
+  };
+  auto epilogue = [&](int64_t r, const double (&q)[CPL], const double (&pd)[CPL]) {
+    if (r < a.n) stg4(a.Q + r * K + col, q);
+    const int c0 = cl * CPL;
+    *reinterpret_cast<double2*>(sp + rr * SS + scr_col<W>(c0)) = make_double2(pd[0], pd[1]);
+    *reinterpret_cast<double2*>(sp + rr * SS + scr_col<W>(c0 + 2)) = make_double2(pd[2], pd[3]);
+    *reinterpret_cast<double2*>(sq + rr * SS + scr_col<W>(c0)) = make_double2(q[0], q[1]);
+    *reinterpret_cast<double2*>(sq + rr * SS + scr_col<W>(c0 + 2)) = make_double2(q[2], q[3]);
+    __syncwarp();
+#pragma unroll
+    for (int cc = 0; cc < RPW / 4; ++cc) {
+      const int sr = (4 * cc + (lane & 3)) * SS;
+#pragma unroll
+      for (int pi = 0; pi < L::NPAIR; ++pi) {
+        int at, bt;
+        wide_pair<K, P, W, CPL>(pi, at, bt);
+        double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
+        dmma(d, sp[sr + scr_col<W>(at * 8 + (lane >> 2))],
+             sq[sr + scr_col<W>(bt * 8 + (lane >> 2))]);
+        acc[2 * pi] = d[0];
+        acc[2 * pi + 1] = d[1];
+      }
+    }
+    __syncwarp();
+  };
+
+  // Pipeline: slice s (chunk + tri loaded), s1 (extent loaded); the slice
+  // after a run's last one is the first of the warp's next super tile.
+  auto next_of = [&](int64_t s) { return (s % LR) + 1 < LR ? s + 1 : s + 1 - LR + wstride * LR; };
+  int64_t s = sup * LR;
+  int64_t s1 = next_of(s);
+  int64_t b0, b1;
+  int w0, w1;
+  double v[CH], td[4], xm[CPL], xc[CPL];
+  int c[CH];
+  extent(s, b0, w0);
+  extent(s1, b1, w1);
+  load_chunk(b0, 0, w0, v, c);
+  load_tri(s, td);
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) xm[t] = xc[t] = 0.0;
+#pragma unroll 1
+  for (; sup < nsup; sup += wstride) {
+    const int64_t base = sup * (RPW * LR) + rr * LR;
+#pragma unroll 1
+    for (int t = 0; t < LR; ++t) {
+      const int64_t row = base + t;
+      if (t == 0) {  // run start: window P[row - 1], P[row]
+        load_row(row - 1, xm);
+        load_row(row, xc);
+      }
+      double xp[CPL];
+      load_row(row + 1, xp);
+      const int64_t s2 = next_of(s1);
+      int64_t b2;
+      int w2;
+      extent(s2, b2, w2);
+      double nv[CH], nt[4];
+      int nc[CH];
+      load_chunk(b1, 0, w1, nv, nc);
+      load_tri(s1, nt);
+      double q[CPL];
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) q[e] = 0.0;
+      gather_fma(v, c, q);
+      for (int off = CH; off < w0; off += CH) {  // slices wider than one chunk
+        double v2[CH];
+        int c2[CH];
+        load_chunk(b0, off, w0, v2, c2);
+        gather_fma(v2, c2, q);
+      }
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) {
+        q[e] = fma(td[0], xm[e], q[e]);
+        q[e] = fma(td[1], xc[e], q[e]);
+        q[e] = fma(td[2], xp[e], q[e]);
+      }
+      epilogue(row, q, xc);
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) {
+        xm[e] = xc[e];
+        xc[e] = xp[e];
+      }
+      s = s1;
+      s1 = s2;
+      b0 = b1;
+      w0 = w1;
+      b1 = b2;
+      w1 = w2;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        v[u] = nv[u];
+        c[u] = nc[u];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) td[e] = nt[e];
+    }
+  }
+  __syncthreads();  // the scratch is reused as the reduction buffer
+  double* red = sm;
+  if (!grid_reduce<L::TPR, L::NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group))
+    return;
+  double* alpha = sm + L::RED;
+  double* ws = alpha + 3 * S::CS;
+  gather_gram_wide<K, P, W, CPL, GLOBAL>(red, alpha);
+  __syncthreads();
+  if (a.dist) {
+    for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
+    return;
+  }
+  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
+}
+
 // Dynamic shared memory of k1_wide: max(warp scratch, reduction epilogue).
 template <int K, int P, int W, int CPL, bool GLOBAL>
 int k1_wide_smem() {
