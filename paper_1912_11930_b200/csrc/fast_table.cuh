@@ -40,7 +40,7 @@ constexpr int k1w_chunk() {
 // chunk (slots left after the r-1, r, r+1 entries are taken out: 4 on a
 // 7-point stencil, 2 on a 5-point one).
 #ifndef BKG_K1L_RUN
-#define BKG_K1L_RUN 32
+#define BKG_K1L_RUN 64
 #endif
 #ifndef BKG_K1L_CH
 #define BKG_K1L_CH 4
