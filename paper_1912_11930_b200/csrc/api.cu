@@ -516,6 +516,8 @@ bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
   const char* env = std::getenv("BKG_K1_LINE");
   if (env && env[0] == '0') return false;
   const bool forced = env && env[0] == '1';
+  if (forced) return true;
+  if (!ft.line_auto) return false;
   if (A->tri_nnz < 0) {
     DevBuf<unsigned long long> cnt(1);
     BKG_CUDA_CHECK(cudaMemsetAsync(cnt.ptr, 0, sizeof(unsigned long long), c->stream));
@@ -530,8 +532,6 @@ bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
     sync(c);
     A->tri_nnz = (int64_t)h;
   }
-  if (forced) return true;
-  if (!ft.line_auto) return false;
   if ((double)A->tri_nnz < 0.2 * (double)A->nnz) return false;
   int nb = 0;
   allow_smem(ft.k1_line, ft.smem_k1);
