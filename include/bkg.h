@@ -141,6 +141,18 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
               const double* b, const double* x0, const bkg_solve_options* opts, double* x_out,
               double* history, uint64_t history_cap, double* final_norms, bkg_report* rep);
 
+/* Defect history of the context's last bkg_solve (rows x k doubles): the
+ * reference grows defect_history one row per iteration (solver.hpp:146,198),
+ * so callers size their buffer after the solve from *rows instead of from
+ * max_iter.  Copies min(cap, rows) rows; history may be NULL to query.      */
+int bkg_solve_history(bkg_ctx* ctx, double* history, uint64_t cap, uint64_t* rows);
+
+/* Which K1 (SpMM + alpha Gram) the context's last bkg_solve ran: -1 exact /
+ * unfused kernels, 0 k1_wide (sliced ELL), 1 k1_line (line-window sliced
+ * ELL), 2 k1_stage (TMA-staged row blocks).  Tests assert the headline
+ * configs run the kernel the bench measures.                                */
+int bkg_solve_k1_variant(bkg_ctx* ctx, int* variant);
+
 /* ---- device-resident solver (bench / repeated solves) ------------------- */
 /* Keeps A, B, X and the work block vectors resident in HBM.                */
 int bkg_solver_create(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mode,
@@ -153,6 +165,8 @@ int bkg_solver_run(bkg_solver* s, double tol, uint64_t max_iter, int record_hist
                    bkg_report* rep);
 int bkg_solver_get_x(bkg_solver* s, double* x_host);
 int bkg_solver_history(bkg_solver* s, double* history, uint64_t cap, uint64_t* rows);
+/* K1 variant of a resident solver (same codes as bkg_solve_k1_variant).     */
+int bkg_solver_k1_variant(const bkg_solver* s, int* variant);
 /* Device time (ms, CUDA events on the solver stream) of each fused kernel
  * class averaged over `iterations` iterations of an untimed profiling pass:
  * out_ms[0]=SpMM+Gram (K1), [1]=update+Gram (K2), [2]=P update (K3),

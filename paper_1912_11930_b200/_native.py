@@ -103,6 +103,9 @@ SIGNATURES = [
     ("bkg_solver_run", C.c_int, [_vp, C.c_double, C.c_uint64, C.c_int, C.POINTER(Report)]),
     ("bkg_solver_get_x", C.c_int, [_vp, _d]),
     ("bkg_solver_history", C.c_int, [_vp, _d, C.c_uint64, _u]),
+    ("bkg_solve_history", C.c_int, [_vp, _d, C.c_uint64, _u]),
+    ("bkg_solve_k1_variant", C.c_int, [_vp, C.POINTER(C.c_int)]),
+    ("bkg_solver_k1_variant", C.c_int, [_vp, C.POINTER(C.c_int)]),
     ("bkg_solver_profile", C.c_int, [_vp, C.c_uint64, _d]),
     ("bkg_solver_debug_first_step", C.c_int, [_vp, _d, _d]),
     ("bkg_solver_kernel_bytes", C.c_int, [_vp, _d]),

@@ -115,6 +115,14 @@ class Context:
         _check(N.lib().bkg_ctx_launch_count(self.handle, C.byref(v)))
         return v.value
 
+    K1_VARIANTS = {-1: "exact", 0: "k1_wide", 1: "k1_line", 2: "k1_stage"}
+
+    def last_k1(self) -> str:
+        """K1 kernel of this context's last bcg_solve (bkg_solve_k1_variant)."""
+        v = C.c_int()
+        _check(N.lib().bkg_solve_k1_variant(self.handle, C.byref(v)))
+        return self.K1_VARIANTS[v.value]
+
     def adopt(self, obj) -> None:
         """Register a native object bound to this context (it is closed first
         when the context closes, so nothing outlives its bkg_ctx)."""
@@ -615,10 +623,6 @@ def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None,
         x = out
     else:
         x = np.empty_like(b)
-    max_iter = opts.max_iter or 10 * n
-    cap = (max_iter + 1) if opts.record_history else 0
-    cap = min(cap, max(1, (1 << 28) // max(k, 1)))
-    hist = np.empty((max(cap, 1), k))
     fin = np.empty(k)
     rep = N.Report()
     so = N.SolveOptions()
@@ -641,7 +645,7 @@ def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None,
         so.on_iterate = cb_holder
     x0p = _dp(x0) if x0 is not None else None
     st = N.lib().bkg_solve(ctx.handle, a.device(ctx), cfg.k, cfg.p, cfg._mode_code, _dp(b), x0p,
-                           C.byref(so), _dp(x), _dp(hist), cap, _dp(fin), C.byref(rep))
+                           C.byref(so), _dp(x), None, 0, _dp(fin), C.byref(rep))
     _check(st)
     if errors:
         raise errors[0]
@@ -655,9 +659,12 @@ def bcg_solve(a: SparseMatrix, b, *args, ctx: Optional[Context] = None,
         loop_seconds=float(rep.loop_seconds))
     if rep.breakdown:
         report.breakdown = BreakdownInfo(int(rep.breakdown_iteration), int(rep.breakdown_block))
-    if opts.record_history:
-        rows = min(int(rep.history_rows), cap)
-        report.defect_history = [hist[i].copy() for i in range(rows)]
+    if opts.record_history:  # sized from the rows produced (solver.hpp:146,198)
+        rows = int(rep.history_rows)
+        hist = np.empty((max(rows, 1), k))
+        got = C.c_uint64(0)
+        _check(N.lib().bkg_solve_history(ctx.handle, _dp(hist), rows, C.byref(got)))
+        report.defect_history = [hist[i].copy() for i in range(min(rows, got.value))]
     return SolveResult(x, report)
 
 

@@ -579,6 +579,7 @@ struct bkg_solver {
 
   cudaGraphExec_t graph = nullptr;  // `chunk` fused iterations, captured once
   IterArgs graph_args{};            // the arguments baked into `graph`
+  uint64_t graph_kernels = 0;       // kernel nodes in `graph`
 
   ~bkg_solver() {
     if (graph) cudaGraphExecDestroy(graph);
@@ -602,13 +603,14 @@ struct bkg_solver {
       BKG_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
       const uint64_t before = ctx->launches;
       for (int i = 0; i < chunk; ++i) launch_iteration(true);
+      graph_kernels = ctx->launches - before;  // kernels per replay (8 per ILU(0) iteration)
       ctx->launches = before;
       BKG_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
       BKG_CUDA_CHECK(cudaGraphInstantiate(&graph, g, 0));
       cudaGraphDestroy(g);
     }
     BKG_CUDA_CHECK(cudaGraphLaunch(graph, ctx->stream));
-    ctx->launches += 3ull * chunk;
+    ctx->launches += graph_kernels;
   }
 
   void init(bkg_ctx* c, const bkg_matrix* a, int kk, int pp, bool gl,
@@ -643,12 +645,7 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
-      if (use_line(c, A, ft)) {
-        ft.k1 = ft.k1_line;
-        ft.rpc_k1 = ft.rpc_k1_line;
-        k1_run = ft.line_run;
-      }
-      g1 = occupancy_grid(c, ft.k1, ft.smem_k1, n, ft.rpc_k1);
+      choose_k1();
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
       pcx = jac ? 1 : (precond == BKG_PRECOND_ILU0 ? 2 : 0);
@@ -666,6 +663,38 @@ struct bkg_solver {
       }
       partials.alloc((size_t)gmax * ft.e_iter);
       gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
+    }
+  }
+
+  int k1_variant() const { return !fast ? -1 : k1_run > 0 ? 1 : 0; }
+
+  // Per-matrix K1 choice (k1_line or k1_wide) and its grid.
+  void choose_k1() {
+    FastTable base;
+    use_fast(ctx, k, p, global, &base);
+    ft.k1 = base.k1;
+    ft.rpc_k1 = base.rpc_k1;
+    k1_run = 0;
+    if (use_line(ctx, A, ft)) {
+      ft.k1 = ft.k1_line;
+      ft.rpc_k1 = ft.rpc_k1_line;
+      k1_run = ft.line_run;
+    }
+    g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, n, ft.rpc_k1);
+  }
+
+  // A cached workspace reused for another matrix of the same shape: redo the
+  // per-matrix choices so the kernel (and fast-mode summation order) depends
+  // on the matrix solved, not on call history.
+  void bind_matrix(const bkg_matrix* a) {
+    if (a == A) return;
+    A = a;
+    if (!fast) return;
+    choose_k1();
+    if (partials.count < (size_t)g1 * ft.e_iter) partials.alloc((size_t)g1 * ft.e_iter);
+    if (graph) {
+      cudaGraphExecDestroy(graph);
+      graph = nullptr;
     }
   }
 
@@ -1126,6 +1155,11 @@ int bkg_matrix_create(bkg_ctx* ctx, uint64_t n, const uint64_t* off, const uint6
     BKG_REQUIRE(off[0] == 0, BKG_CONFIG, "sparse matrix: offsets inconsistent with stored entries");
     const uint64_t nnz = off[n];
     BKG_REQUIRE(nnz < (1ull << 40), BKG_CONFIG, "sparse matrix: offsets inconsistent with stored entries");
+    // the device conversion walks [off[r], off[r+1]): check on the host that
+    // every extent lies inside [0, nnz] before anything reads it
+    for (uint64_t r = 0; r < n; ++r)
+      BKG_REQUIRE(off[r] <= off[r + 1] && off[r + 1] <= nnz, BKG_CONFIG,
+                  "sparse matrix: row_offsets must be non-decreasing");
     activate(ctx);
     auto* m = new bkg_matrix();
     m->ctx = ctx;
@@ -1560,7 +1594,7 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
       cached->init(ctx, a, (int)k, (int)p, mode == BKG_GLOBAL, opts->precond);
     }
     bkg_solver& s = *cached;
-    s.A = a;
+    s.bind_matrix(a);
     s.precond = opts->precond;
     s.timing = opts->time_kernels != 0;
     h2d(ctx, s.B.ptr, b, (size_t)a->n * k);
@@ -1573,6 +1607,28 @@ int bkg_solve(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, uint64_t p, int mod
       const uint64_t r = std::min<uint64_t>(history_cap, s.history_rows);
       std::memcpy(history, s.history.data(), r * k * sizeof(double));
     }
+  });
+}
+
+int bkg_solve_k1_variant(bkg_ctx* ctx, int* variant) {
+  return guard([&] {
+    const bkg_solver* s = static_cast<const bkg_solver*>(ctx->solver_cache);
+    BKG_REQUIRE(s != nullptr, BKG_CONFIG, "no solve has run on this context");
+    *variant = s->k1_variant();
+  });
+}
+
+int bkg_solver_k1_variant(const bkg_solver* s, int* variant) {
+  return guard([&] { *variant = s->k1_variant(); });
+}
+
+int bkg_solve_history(bkg_ctx* ctx, double* history, uint64_t cap, uint64_t* rows) {
+  return guard([&] {
+    const bkg_solver* s = static_cast<const bkg_solver*>(ctx->solver_cache);
+    const uint64_t have = s ? s->history_rows : 0;
+    if (rows) *rows = have;
+    if (history && s)
+      std::memcpy(history, s->history.data(), std::min(cap, have) * s->k * sizeof(double));
   });
 }
 

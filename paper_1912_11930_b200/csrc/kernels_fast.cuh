@@ -571,9 +571,14 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
             const int e = b * P + (col0 + j) % P;
-            if constexpr (XM == 2) xv[u][j] = fma(os, og[e], xv[u][j]);
-            xv[u][j] = fma(ps, lg[e], xv[u][j]);
-            pn[j] = fma(ps, bg[e], pn[j]);
+            if constexpr (XM == 2)
+              if (old) xv[u][j] = fma(os, og[e], xv[u][j]);
+            // after a lambda breakdown (cur = 0) lg / bg hold stale values
+            // (an Inf there must not reach X): skip, as k3_mma does
+            if (cur) {
+              xv[u][j] = fma(ps, lg[e], xv[u][j]);
+              pn[j] = fma(ps, bg[e], pn[j]);
+            }
           }
         }
       }

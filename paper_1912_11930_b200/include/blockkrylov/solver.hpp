@@ -93,10 +93,7 @@ inline SolveResult bcg_solve(const SparseMatrix& a, const BlockVector& b, const 
   if (!(opts.tol > 0.0)) throw ConfigError("bcg_solve: tol must be positive");
 
   const std::size_t n = b.rows(), k = b.cols();
-  const std::size_t max_iter = opts.max_iter ? opts.max_iter : 10 * n;
   SolveResult res{BlockVector(n, k), {}};
-  const std::size_t cap = opts.record_history ? max_iter + 1 : 0;
-  std::vector<double> hist(opts.record_history ? cap * k : 0);
   res.report.final_defect_norms.assign(k, 0.0);
   detail::ObserverBridge bridge{&opts, {}, {}};
   bkg_solve_options o{};
@@ -111,7 +108,7 @@ inline SolveResult bcg_solve(const SparseMatrix& a, const BlockVector& b, const 
   }
   bkg_report rep{};
   detail::check(bkg_solve(gpu::context(), a.device(), cfg.k(), cfg.p(), cfg.abi_mode(), b.data(),
-                          x0.data(), &o, res.x.data(), hist.data(), cap,
+                          x0.data(), &o, res.x.data(), nullptr, 0,
                           res.report.final_defect_norms.data(), &rep));
   SolveReport& r = res.report;
   r.iterations = rep.iterations;
@@ -120,9 +117,14 @@ inline SolveResult bcg_solve(const SparseMatrix& a, const BlockVector& b, const 
   r.seconds = {rep.seconds_bdot, rep.seconds_baxpy, rep.seconds_bop, rep.seconds_precond};
   r.loop_seconds = rep.loop_seconds;
   if (rep.breakdown) r.breakdown = BreakdownInfo{rep.breakdown_iteration, rep.breakdown_block};
-  const std::size_t rows = std::min<std::size_t>(rep.history_rows, cap);
-  for (std::size_t i = 0; i < rows; ++i)
-    r.defect_history.emplace_back(hist.begin() + i * k, hist.begin() + (i + 1) * k);
+  if (opts.record_history) {  // sized from the rows the solve produced, not max_iter
+    const std::size_t rows = rep.history_rows;
+    std::vector<double> hist(rows * k);
+    uint64_t got = 0;
+    detail::check(bkg_solve_history(gpu::context(), hist.data(), rows, &got));
+    for (std::size_t i = 0; i < rows && i < got; ++i)
+      r.defect_history.emplace_back(hist.begin() + i * k, hist.begin() + (i + 1) * k);
+  }
   return res;
 }
 

@@ -40,6 +40,12 @@ class DeviceSolver:
         code = {"uniform": 0, "normal": 1}[distribution]
         _check(N.lib().bkg_solver_generate_rhs(self.handle, code, seed))
 
+    def k1(self) -> str:
+        """K1 kernel this solver runs (bkg_solver_k1_variant)."""
+        v = C.c_int()
+        _check(N.lib().bkg_solver_k1_variant(self.handle, C.byref(v)))
+        return Context.K1_VARIANTS[v.value]
+
     def run(self, tol: float = 1e-8, max_iter: int = 0, record_history: bool = False) -> N.Report:
         rep = N.Report()
         _check(N.lib().bkg_solver_run(self.handle, tol, max_iter, int(record_history),

@@ -114,6 +114,9 @@ FULL_CASES = [
          coeff_seed=COEFF_SEED),
     Case("c3_full_global4", DIFFUSION2D_LOGNORMAL, 1024, 1024, 1, 64, 4, True, "uniform",
          coeff_seed=COEFF_SEED),
+    # C5 at 128^3 (n = 2,097,152): k=64, hybrid p=16, 100 iterations -- large
+    # enough that the solver auto-selects k1_line, the kernel of the C5 headline
+    Case("c5_full_128", LAPLACE3D_7PT, 128, 128, 128, 64, 16, False, "normal", 1e-8, 100),
 ]
 
 BY_NAME = {c.name: c for c in CASES + FULL_CASES}

@@ -15,7 +15,16 @@ def load(name):
 
 
 def names(full=False):
-    """Fixture names; full-size BASELINE configs only when full=True."""
+    """Fixture names.  full=True returns EVERY full-size case declared in
+    cases.FULL_CASES whether or not its fixture exists, so a missing fixture
+    fails its test (load() raises) instead of silently dropping out."""
     from cases import FULL_NAMES
+    if full:
+        return sorted(FULL_NAMES)
     all_ = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
-    return [n for n in all_ if (n in FULL_NAMES) == full]
+    return [n for n in all_ if n not in FULL_NAMES]
+
+
+def missing_full():
+    """FULL_CASES whose fixture has not been generated."""
+    return [n for n in names(full=True) if not os.path.exists(os.path.join(GOLDEN, f"{n}.npz"))]

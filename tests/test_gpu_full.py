@@ -43,6 +43,7 @@ def solve(name, numerics):
                        bk.SubalgebraConfig(case.k, case.p, case.mode),
                        bk.SolveOptions(tol=case.tol, max_iter=case.max_iter, record_history=True),
                        ctx=ctx)
+    res.k1 = ctx.last_k1()
     a.release_device()
     ctx.close()
     return res, g
@@ -63,6 +64,11 @@ def test_full_exact_bit_identical(name):
     assert hashlib.sha256(res.x.tobytes()).hexdigest() == m["x_sha256"]
 
 
+def test_full_fixtures_present():
+    """Every FULL_CASES fixture exists (a missing one is a failure, not a skip)."""
+    assert golden_io.missing_full() == []
+
+
 @pytest.mark.parametrize("name", FULL)
 def test_full_fast_parity_bars(name):
     res, g = solve(name, "fast")
@@ -75,6 +81,8 @@ def test_full_fast_parity_bars(name):
     xerr = np.max(np.abs(xs - g["x_sample"])) / np.max(np.abs(g["x_sample"]))
     assert int(r.converged) == m["converged"]
     assert xerr <= 1e-8, xerr
+    if name.startswith("c5_full"):  # the C5 headline's K1 (the one bench.py times)
+        assert res.k1 in ("k1_line", "k1_stage"), res.k1
     if name.startswith("c3_full"):  # reorder-chaotic field (floor case)
         assert abs(r.iterations - m["iterations"]) <= max(1, int(0.05 * m["iterations"]))
     else:
