@@ -204,6 +204,20 @@ int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
                             const uint64_t* cols, const double* vals, uint64_t k, uint64_t p,
                             int mode, int rank, int nranks, const void* nccl_id,
                             bkg_psolver** out);
+/* Same, with this rank's rows [row_begin, row_end) of a stencil matrix
+ * (kinds and seeds of bkg_matrix_generate) generated on its own device: no
+ * host CSR, no global assembly (C5 at 384^3: 6.2 GB of CSR, 29 GB per block
+ * vector).                                                                  */
+int bkg_psolver_create_nccl_generated(bkg_ctx* ctx, int kind, uint64_t nx, uint64_t ny,
+                                      uint64_t nz, uint64_t seed, double contrast,
+                                      uint64_t row_begin, uint64_t row_end, uint64_t k,
+                                      uint64_t p, int mode, int rank, int nranks,
+                                      const void* nccl_id, bkg_psolver** out);
+/* Fill each part's B with its rows of the generated block (distribution as
+ * bkg_solver_generate_rhs); bkg_psolver_get_rhs reads it back (virtual:
+ * global n*k; NCCL: this rank's rows).                                      */
+int bkg_psolver_generate_rhs(bkg_psolver* s, int distribution, uint64_t seed);
+int bkg_psolver_get_rhs(bkg_psolver* s, double* b);
 int bkg_psolver_destroy(bkg_psolver* s);
 /* virtual: global B (n*k); NCCL: this rank's rows.                         */
 int bkg_psolver_set_rhs(bkg_psolver* s, const double* b);

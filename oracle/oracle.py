@@ -94,6 +94,10 @@ class Oracle:
         f("bench_solve").argtypes = [C.c_int, _sz, _up, _up, _dp, _sz, _sz, C.c_int, _dp,
                                      C.c_double, _u64, C.POINTER(C.c_uint64)]
         f("bench_solve").restype = C.c_double
+        if kind == "reference":
+            L.bkref_bench_iterations.argtypes = [C.c_int, _sz, _up, _up, _dp, _sz, _sz, C.c_int,
+                                                 _dp, _u64, C.POINTER(C.c_uint64)]
+            L.bkref_bench_iterations.restype = C.c_double
         if kind == "port":
             L.orc_normal_block_rhs.argtypes = [_sz, _sz, _u64, _dp]
             L.orc_stencil_nnz.argtypes = [C.c_int, _sz, _sz, _sz]
@@ -213,6 +217,17 @@ class Oracle:
         its = C.c_uint64(0)
         dt = self._f("bench_solve")(threads, n, rp, cols, vals, k, p, int(glob),
                                     np.ascontiguousarray(b), tol, max_iter, C.byref(its))
+        return dt, int(its.value)
+
+
+    def bench_iterations(self, threads, csr, b, p, glob, iters):
+        """Reference only: seconds of `threads` concurrent solves' iterations
+        1..iters, setup and final residual excluded (observer-timed)."""
+        rp, cols, vals = csr
+        n, k = b.shape
+        its = C.c_uint64(0)
+        dt = self.lib.bkref_bench_iterations(threads, n, rp, cols, vals, k, p, int(glob),
+                                             np.ascontiguousarray(b), iters, C.byref(its))
         return dt, int(its.value)
 
 

@@ -8,7 +8,10 @@
 // copy of reference source: it only #includes the reference headers.
 #include <blockkrylov/blockkrylov.hpp>
 
+#include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdint>
 #include <cstring>
 #include <thread>
@@ -192,6 +195,58 @@ double bkref_bench_solve(int threads, size_t n, const uint64_t* rowptr, const ui
   const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   uint64_t total = 0;
   for (auto v : its) total += v;
+  if (iterations) *iterations = total;
+  return dt;
+}
+
+// CPU baseline with the loop isolated: `threads` concurrent reference solves
+// of the same system, max_iter = iters, tol tiny.  The reference calls
+// SolveOptions::on_iterate at i = 0 after its setup (solver.hpp:147) and after
+// every iteration (:199); the observer holds every thread at i = 0 until all
+// threads are there, so the window [release, last thread's i = iters] is
+// `threads` x `iters` concurrent reference iterations -- no per-solve setup,
+// no final residual.  Returns the window in seconds.
+double bkref_bench_iterations(int threads, size_t n, const uint64_t* rowptr, const uint64_t* cols,
+                              const double* vals, size_t k, size_t p, int global,
+                              const double* b, uint64_t iters, uint64_t* iterations) {
+  const SparseMatrix a = to_csr(n, rowptr, cols, vals);
+  const SubalgebraConfig cfg = make_cfg(k, p, global);
+  const BlockVector bv = to_bv(n, k, b);
+  const Preconditioner m = Preconditioner::identity(n);
+  if (threads < 1) threads = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  std::chrono::steady_clock::time_point start;
+  std::vector<std::chrono::steady_clock::time_point> end(threads);
+  std::vector<uint64_t> its(threads, 0);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      SolveOptions opts;
+      opts.tol = 1e-300;
+      opts.max_iter = iters;
+      opts.on_iterate = [&, t](std::size_t i, const BlockVector&, const BlockVector&) {
+        if (i == 0) {
+          std::unique_lock<std::mutex> lk(mu);
+          if (++arrived == threads) {
+            start = std::chrono::steady_clock::now();
+            cv.notify_all();
+          } else {
+            cv.wait(lk, [&] { return arrived == threads; });
+          }
+        }
+        if (i == iters) end[t] = std::chrono::steady_clock::now();
+      };
+      its[t] = bcg_solve(a, bv, m, cfg, opts).report.iterations;
+    });
+  for (auto& th : pool) th.join();
+  double dt = 0.0;
+  uint64_t total = 0;
+  for (int t = 0; t < threads; ++t) {
+    dt = std::max(dt, std::chrono::duration<double>(end[t] - start).count());
+    total += its[t];
+  }
   if (iterations) *iterations = total;
   return dt;
 }

@@ -16,7 +16,12 @@ void allow_smem(const void* fn, int bytes);
 int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
 // generate.cu: device-side problem generation
-void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst);
+void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
+                      int64_t row0 = 0);
+void dev_generate_stencil_rows(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
+                               uint64_t seed, double contrast, int64_t r0, int64_t r1,
+                               int64_t cshift, int64_t* rowptr, int32_t* cols, double* vals);
+int64_t stencil_rows_nnz(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1);
 void dev_generate_stencil(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
                           uint64_t seed, double contrast, bkg_matrix* m);
 void check_cfg(uint64_t k, uint64_t p, int mode);

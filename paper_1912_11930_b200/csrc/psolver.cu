@@ -118,6 +118,25 @@ __global__ void k_residual_sub(int64_t total, const double* __restrict__ b, doub
     ax[i] = b[i] - ax[i];
 }
 
+// [min, max] of the local columns (atomics on an int2 initialised to
+// {INT_MAX, INT_MIN}).
+__global__ void k_col_range(int64_t nnz, const int32_t* __restrict__ cols, int* mm) {
+  int lo = 0x7fffffff, hi = (int)0x80000000;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    lo = min(lo, cols[i]);
+    hi = max(hi, cols[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
 // ---------------------------------------------------------- halo plan ---
 // Pure host logic (also exported for the multi-process CPU tests): part r
 // needs rows [need_lo[r], need_hi[r]) of the operand; it owns [row_begin[r],
@@ -216,6 +235,36 @@ struct bkg_psolver {
     h2d(ctx, pt.cols.ptr, lc.data(), nnz);
     h2d(ctx, pt.vals.ptr, vals, nnz);
     sync(ctx);
+    parts.push_back(std::move(pt));
+  }
+
+  // Rows [r0, r1) of a stencil matrix generated straight into this part's
+  // device CSR (local columns), no host CSR (SURVEY §8f row 3 at 384^3).
+  void add_part_generated(int kind, int64_t nx, int64_t ny, int64_t nz, uint64_t seed,
+                          double contrast, int64_t r0, int64_t r1) {
+    Part pt;
+    pt.r0 = r0;
+    pt.r1 = r1;
+    pt.nloc = r1 - r0;
+    pt.nnz = stencil_rows_nnz(kind, nx, ny, nz, r0, r1);
+    pt.rowptr.alloc(pt.nloc + 1);
+    pt.cols.alloc(std::max<int64_t>(pt.nnz, 1));
+    pt.vals.alloc(std::max<int64_t>(pt.nnz, 1));
+    dev_generate_stencil_rows(ctx, kind, nx, ny, nz, seed, contrast, r0, r1, r0, pt.rowptr.ptr,
+                              pt.cols.ptr, pt.vals.ptr);
+    DevBuf<int> mm(2);
+    const int init[2] = {0x7fffffff, (int)0x80000000};
+    h2d(ctx, mm.ptr, init, 2);
+    int64_t nz_ = pt.nnz;
+    const int32_t* cp = pt.cols.ptr;
+    int* mp = mm.ptr;
+    void* args[] = {&nz_, &cp, &mp};
+    launch(ctx, (const void*)&k_col_range, elem_grid(ctx, pt.nnz), 256, 0, args);
+    int h[2];
+    d2h(ctx, h, mm.ptr, 2);
+    sync(ctx);
+    pt.lo = std::min(r0, r0 + (int64_t)h[0]);
+    pt.hi = std::max(r1, r0 + (int64_t)h[1] + 1);
     parts.push_back(std::move(pt));
   }
 
@@ -589,10 +638,14 @@ int bkg_psolver_create_virtual(bkg_ctx* ctx, uint64_t n, const uint64_t* rowptr,
   });
 }
 
-int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
-                            uint64_t row_end, const uint64_t* local_rowptr, const uint64_t* cols,
-                            const double* vals, uint64_t k, uint64_t p, int mode, int rank,
-                            int nranks, const void* nccl_id, bkg_psolver** out) {
+}  // extern "C"
+
+namespace {
+// One part per process over NCCL; `add` builds this rank's part.
+template <class Add>
+int create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin, uint64_t row_end, uint64_t k,
+                uint64_t p, int mode, int rank, int nranks, const void* nccl_id,
+                bkg_psolver** out, Add&& add) {
   return pguard([&] {
     *out = nullptr;
     check_cfg(k, p, mode);
@@ -612,7 +665,7 @@ int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       BKG_NCCL_CHECK(nccl().CommInitRank(&s->comm, nranks, id, rank));
-      s->add_part((int64_t)row_begin, (int64_t)row_end, local_rowptr, cols, vals);
+      add(s);
       // exchange [row_begin, row_end, need_lo, need_hi, nnz] of every rank
       DevBuf<int64_t> mine(5), all((size_t)5 * nranks);
       const Part& me = s->parts[0];
@@ -644,6 +697,61 @@ int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
       throw;
     }
     *out = s;
+  });
+}
+}  // namespace
+
+extern "C" {
+
+int bkg_psolver_create_nccl(bkg_ctx* ctx, uint64_t n_global, uint64_t row_begin,
+                            uint64_t row_end, const uint64_t* local_rowptr, const uint64_t* cols,
+                            const double* vals, uint64_t k, uint64_t p, int mode, int rank,
+                            int nranks, const void* nccl_id, bkg_psolver** out) {
+  return create_nccl(ctx, n_global, row_begin, row_end, k, p, mode, rank, nranks, nccl_id, out,
+                     [&](bkg_psolver* s) {
+                       s->add_part((int64_t)row_begin, (int64_t)row_end, local_rowptr, cols,
+                                   vals);
+                     });
+}
+
+int bkg_psolver_create_nccl_generated(bkg_ctx* ctx, int kind, uint64_t nx, uint64_t ny,
+                                      uint64_t nz, uint64_t seed, double contrast,
+                                      uint64_t row_begin, uint64_t row_end, uint64_t k,
+                                      uint64_t p, int mode, int rank, int nranks,
+                                      const void* nccl_id, bkg_psolver** out) {
+  if (kind < 0 || kind > 4) {
+    set_error("stencil: unknown kind");
+    return BKG_CONFIG;
+  }
+  if (kind <= 2) nz = 1;
+  uint64_t n = 0, nnz = 0;
+  bkg_stencil_size(kind, nx, ny, nz, &n, &nnz);
+  return create_nccl(ctx, n, row_begin, row_end, k, p, mode, rank, nranks, nccl_id, out,
+                     [&](bkg_psolver* s) {
+                       s->add_part_generated(kind, (int64_t)nx, (int64_t)ny, (int64_t)nz, seed,
+                                             contrast, (int64_t)row_begin, (int64_t)row_end);
+                     });
+}
+
+int bkg_psolver_generate_rhs(bkg_psolver* s, int distribution, uint64_t seed) {
+  return pguard([&] {
+    BKG_REQUIRE(distribution == 0 || distribution == 1, BKG_CONFIG, "unknown RHS distribution");
+    activate(s->ctx);
+    for (Part& pt : s->parts)
+      dev_generate_rhs(s->ctx, distribution, pt.nloc, s->k, seed, pt.B.ptr, pt.r0);
+    sync(s->ctx);
+    s->have_b = true;
+  });
+}
+
+int bkg_psolver_get_rhs(bkg_psolver* s, double* b) {
+  return pguard([&] {
+    activate(s->ctx);
+    for (Part& pt : s->parts) {
+      const int64_t off = s->use_nccl ? 0 : pt.r0;
+      d2h(s->ctx, b + (size_t)off * s->k, pt.B.ptr, (size_t)pt.nloc * s->k);
+    }
+    sync(s->ctx);
   });
 }
 

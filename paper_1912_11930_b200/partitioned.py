@@ -96,6 +96,37 @@ class PartitionedSolver:
                                                cfg._mode_code, rank, nranks, idb, C.byref(h)))
         return PartitionedSolver(h, ctx, n_global, cfg.k, (r0, r1), False)
 
+    @staticmethod
+    def nccl_generated(kind: int, nx: int, ny: int, nz: int, r0: int, r1: int,
+                       cfg: SubalgebraConfig, rank: int, nranks: int, nccl_id: bytes,
+                       ctx: Optional[Context] = None, rhs: Optional[str] = "normal",
+                       seed: int = 7, coeff_seed: int = 0,
+                       contrast: float = 2.0) -> "PartitionedSolver":
+        """One rank's rows [r0, r1) of a stencil matrix generated on its own
+        device (bkg_psolver_create_nccl_generated); B's rows generated there
+        too when rhs is "normal" / "uniform" (bkg_psolver_generate_rhs)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        idb = C.create_string_buffer(nccl_id, 128)
+        _check(N.lib().bkg_psolver_create_nccl_generated(
+            ctx.handle, kind, nx, ny, nz, coeff_seed, contrast, r0, r1, cfg.k, cfg.p,
+            cfg._mode_code, rank, nranks, idb, C.byref(h)))
+        n = nx * ny * (nz if kind >= 3 else 1)
+        s = PartitionedSolver(h, ctx, n, cfg.k, (r0, r1), False)
+        if rhs is not None:
+            s.generate_rhs(rhs, seed)
+        return s
+
+    def generate_rhs(self, distribution: str = "normal", seed: int = 7) -> None:
+        d = {"uniform": 0, "normal": 1}[distribution]
+        _check(N.lib().bkg_psolver_generate_rhs(self.handle, d, seed))
+
+    def rhs(self) -> np.ndarray:
+        rows = self.rows[1] - self.rows[0]
+        out = np.empty((rows, self.k))
+        _check(N.lib().bkg_psolver_get_rhs(self.handle, _dp(out)))
+        return out
+
     def set_rhs(self, b: np.ndarray) -> None:
         b = np.ascontiguousarray(b, dtype=np.float64)
         _check(N.lib().bkg_psolver_set_rhs(self.handle, _dp(b)))
@@ -108,9 +139,11 @@ class PartitionedSolver:
                                        _dp(fin) if final_norms else None, C.byref(rep)))
         return rep, fin
 
-    def x(self) -> np.ndarray:
+    def x(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         rows = self.rows[1] - self.rows[0]
-        out = np.empty((rows, self.k))
+        if out is None:
+            out = np.empty((rows, self.k))
+        assert out.shape == (rows, self.k) and out.dtype == np.float64 and out.flags.c_contiguous
         _check(N.lib().bkg_psolver_get_x(self.handle, _dp(out)))
         return out
 

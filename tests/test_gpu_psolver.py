@@ -95,3 +95,44 @@ def test_partitioned_breakdown_and_maxiter(ctx):
     rep, _ = s.run(1e-30, 5)
     assert rep.iterations == 5 and not rep.converged
     s.close()
+
+
+def test_generated_slab_rhs_matches_host_generator(ctx):
+    """bkg_psolver_generate_rhs: every part generates its rows of B with the
+    stream jumped to its first row -- U(-1,1) bit-identical to the host
+    random_block_rhs over all n rows."""
+    case, a, b = inputs("c2_24")
+    s = PartitionedSolver.virtual(a, bk.SubalgebraConfig(32, 8), 3, ctx)
+    s.generate_rhs("uniform", 7)
+    assert s.rhs().tobytes() == bk.random_block_rhs(a.n(), 32, 7).tobytes()
+    s.generate_rhs("normal", 7)
+    np.testing.assert_allclose(s.rhs(), bk.normal_block_rhs(a.n(), 32, 7), rtol=1e-13, atol=1e-13)
+    s.close()
+
+
+@pytest.mark.parametrize("kind,grid,k,p", [(3, (24, 20, 18), 32, 8), (4, (14, 12, 13), 16, 4),
+                                           (2, (40, 36, 1), 64, 1)])
+def test_nccl_generated_matches_host_csr(ctx, kind, grid, k, p):
+    """One rank, device-generated CSR (bkg_psolver_create_nccl_generated) vs
+    the host CSR of the same stencil: same kernels, same bits."""
+    nx, ny, nz = grid
+    a = bk.stencil(kind, nx, ny, nz, seed=11 if kind == 2 else 0)
+    n = a.n()
+    cfg = bk.SubalgebraConfig(k, p)
+    g = PartitionedSolver.nccl_generated(kind, nx, ny, nz, 0, n, cfg, 0, 1, nccl_unique_id(), ctx,
+                                         rhs="uniform", seed=7,
+                                         coeff_seed=11 if kind == 2 else 0)
+    b = g.rhs()
+    assert b.tobytes() == bk.random_block_rhs(n, k, 7).tobytes()
+    rep, _ = g.run(1e-300, 12, record_history=True)
+    xg, hg = g.x(), g.history(rep.history_rows)
+    g.close()
+    lrp, cols, vals = local_csr(a, 0, n)
+    h = PartitionedSolver.nccl(n, 0, n, lrp, cols, vals, cfg, 0, 1, nccl_unique_id(), ctx)
+    h.set_rhs(b)
+    rep1, _ = h.run(1e-300, 12, record_history=True)
+    assert rep.iterations == rep1.iterations == 12
+    assert rep.flops_bop == rep1.flops_bop
+    assert hg.tobytes() == h.history(rep1.history_rows).tobytes()
+    assert xg.tobytes() == h.x().tobytes()
+    h.close()

@@ -1,8 +1,10 @@
 #!/usr/bin/env python3
 """Summarise an ncu --set full report (per kernel: duration, DRAM bytes,
-throughputs, occupancy, stall mix) into markdown + a traffic JSON used by
-bench.py's roofline.traffic.
-    python tools/ncu_summary.py report.ncu-rep out.md traffic.json"""
+throughputs, occupancy, stall mix) into markdown, and merge the per-launch
+DRAM bytes of each kernel class into profiles/ncu_traffic.json under the
+bench config the report was captured on (bench.py's roofline.traffic reads
+[config][kernel class]).
+    python tools/ncu_summary.py report.ncu-rep out.md traffic.json CONFIG"""
 import csv
 import io
 import json
@@ -16,7 +18,7 @@ def ncu_csv(rep, page):
     return list(csv.reader(io.StringIO(out)))
 
 
-def main(rep, md, tj):
+def main(rep, md, tj, config):
     det = ncu_csv(rep, "details")
     h = det[0]
     ki, mi, vi, ui, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value",
@@ -64,11 +66,17 @@ def main(rep, md, tj):
                else "K3_update_p" if "k3" in name else name)
         traffic.setdefault(key, []).append(p.get("dram_bytes"))
     # per launch; K3 alternates skip / flush launches (deferred X): the mean
-    traffic = {k: sum(v) / len(v) for k, v in traffic.items() if all(x is not None for x in v)}
+    traffic = {k: {"dram_bytes": sum(v) / len(v), "launches": len(v), "source": md}
+               for k, v in traffic.items() if all(x is not None for x in v)}
     open(md, "w").write("\n".join(lines) + "\n")
-    json.dump(traffic, open(tj, "w"), indent=1)
+    try:
+        allt = json.load(open(tj))
+    except (OSError, ValueError):
+        allt = {}
+    allt[config] = traffic
+    json.dump(allt, open(tj, "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
