@@ -541,6 +541,45 @@ bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
   return need >= 2 * (int64_t)std::max(nb, 1) * c->sm_count;
 }
 
+// K1 = k1_stage (TMA-staged blocks, kernels_stage.cuh) when the matrix's
+// blocks fit: the staged-block copy is built once per matrix (stage.cu) and
+// the ring takes as many stages (2..BKG_STAGE_NS, default 6) as fit the
+// shared memory of BKG_STAGE_CTAS (default 1) CTAs per SM.
+// BKG_K1_STAGE=0 turns it off (register-gather K1s).  *ns / *smem out.
+bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem) {
+  if (!ft.k1_stage || A->n == 0) return false;
+  const char* env = std::getenv("BKG_K1_STAGE");
+  if (env && env[0] == '0') return false;
+  const char* line = std::getenv("BKG_K1_LINE");
+  if (line && line[0] == '1') return false;  // an explicit k1_line request wins
+  StageCsr& st = A->stage;
+  if (st.failed_R == ft.stage_R && st.failed_n == (int64_t)A->n) return false;
+  if (st.R != ft.stage_R || st.n != (int64_t)A->n) {
+    if (!stage_build(c, (int64_t)A->n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, ft.stage_R,
+                     32 * kStageSegLanes, st)) {
+      st.failed_R = ft.stage_R;
+      st.failed_n = (int64_t)A->n;
+      return false;
+    }
+  }
+  int optin = 0;
+  BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const char* ec = std::getenv("BKG_STAGE_CTAS");
+  const int ctas = ec ? std::max(1, std::atoi(ec)) : 1;
+  const int per_cta = std::min(optin, (228 * 1024) / ctas - 1024);
+  const char* en = std::getenv("BKG_STAGE_NS");
+  const int nsmax = en ? std::max(2, std::atoi(en)) : 6;
+  for (int q = nsmax; q >= 2; --q) {
+    const int b = ft.stage_smem(st.cap, st.wmax, q);
+    if (b <= per_cta) {
+      *ns = q;
+      *smem = b;
+      return true;
+    }
+  }
+  return false;
+}
+
 // =========================================================== solver =====
 struct bkg_solver {
   bkg_ctx* ctx = nullptr;
@@ -666,16 +705,30 @@ struct bkg_solver {
     }
   }
 
-  int k1_variant() const { return !fast ? -1 : k1_run > 0 ? 1 : 0; }
+  int k1_kind = 0;   // 0 k1_wide, 1 k1_line, 2 k1_stage
+  int stage_ns = 0;  // k1_stage ring depth
 
-  // Per-matrix K1 choice (k1_line or k1_wide) and its grid.
+  int k1_variant() const { return !fast ? -1 : k1_kind; }
+
+  // Per-matrix K1 choice (k1_stage, k1_line or k1_wide) and its grid.
   void choose_k1() {
     FastTable base;
     use_fast(ctx, k, p, global, &base);
     ft.k1 = base.k1;
     ft.rpc_k1 = base.rpc_k1;
+    ft.smem_k1 = base.smem_k1;
     k1_run = 0;
+    k1_kind = 0;
+    int smem = 0;
+    if (use_stage(ctx, A, ft, &stage_ns, &smem)) {
+      k1_kind = 2;
+      ft.k1 = ft.k1_stage;
+      ft.smem_k1 = smem;
+      g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, A->stage.nblk, 1);
+      return;
+    }
     if (use_line(ctx, A, ft)) {
+      k1_kind = 1;
       ft.k1 = ft.k1_line;
       ft.rpc_k1 = ft.rpc_k1_line;
       k1_run = ft.line_run;
@@ -720,7 +773,20 @@ struct bkg_solver {
     a.zsrc = precond == BKG_PRECOND_ILU0 ? Z : nullptr;
     a.Pn = P;
     a.Pold = nullptr;
-    if (fast && ft.sell_rows) {
+    if (fast && k1_kind == 2) {
+      const StageCsr& st = A->stage;
+      a.stg_bseg = st.bseg.ptr;
+      a.stg_bent = st.bent.ptr;
+      a.stg_segs = st.segs.ptr;
+      a.stg_vals = st.vals.ptr;
+      a.stg_lidx = st.lidx.ptr;
+      a.stg_own = st.own.ptr;
+      a.stg_nstage = stage_ns;
+      a.stg_cap = st.cap;
+      a.stg_wmax = st.wmax;
+      a.stg_first1 = 0;
+      a.stg_cnt1 = st.nblk;
+    } else if (fast && ft.sell_rows) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
       // capture: launch_chunk calls iter_args before capturing)
       if (A->sell.rows != ft.sell_rows || A->sell.n != n || A->sell.run != k1_run)

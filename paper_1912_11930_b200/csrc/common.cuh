@@ -136,6 +136,25 @@ struct SellCsr {
   DevBuf<double> vals;
 };
 
+// Staged-block copy of a CSR matrix for k1_stage (kernels_stage.cuh, built by
+// stage.cu): blocks of R consecutive rows; block b stages the row runs
+// segs[bseg[b] .. bseg[b+1]) = {first operand row, rows} into shared memory
+// (own rows start at staged index own[b]); entry (slot u, row i) of block b
+// at bent[b] + u * R + i holds the staged index (lidx, 0xFFFF = padding) and
+// the value of the row's u-th CSR entry.
+struct StageCsr {
+  int R = 0;  // block height (0: not built)
+  int64_t n = 0, nblk = 0;
+  int cap = 0, smax = 0, wmax = 0;  // max staged rows / segments / slots per block
+  int failed_R = 0;                 // a build for (failed_R, failed_n) did not fit
+  int64_t failed_n = 0;
+  DevBuf<int64_t> bseg, bent;
+  DevBuf<int2> segs;
+  DevBuf<uint16_t> lidx;
+  DevBuf<double> vals;
+  DevBuf<int32_t> own;
+};
+
 }  // namespace bkg
 
 struct bkg_matrix;
@@ -172,6 +191,8 @@ struct bkg_matrix {
   bkg::DevBuf<double> vals;
   // sliced-ELL copy for the fused K1 (built lazily by the first fast solve)
   mutable bkg::SellCsr sell;
+  // staged-block copy for k1_stage (built lazily by the first fast solve)
+  mutable bkg::StageCsr stage;
   mutable int64_t tri_nnz = -1;  // entries in columns r - 1 .. r + 1 (counted lazily)
   // preconditioner data (built lazily on device)
   bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)

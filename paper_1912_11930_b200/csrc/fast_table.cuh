@@ -7,6 +7,7 @@
 
 #include "kernels_fast.cuh"
 #include "kernels_k1.cuh"
+#include "kernels_stage.cuh"
 
 // K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
 #ifndef BKG_K1_IMPL
@@ -39,6 +40,10 @@ constexpr int k1w_chunk() {
 // k1_line (line-variant sliced ELL, kernels_k1.cuh): rows per run and CSR
 // chunk (slots left after the r-1, r, r+1 entries are taken out: 4 on a
 // 7-point stencil, 2 on a 5-point one).
+// k1_stage tiles per warp per block (block height = 8 / QW x RPW x TPW rows)
+#ifndef BKG_STAGE_TPW
+#define BKG_STAGE_TPW 1
+#endif
 #ifndef BKG_K1L_RUN
 #define BKG_K1L_RUN 64
 #endif
@@ -78,6 +83,11 @@ struct FastTable {
   int rpc_k1_line = 1;  // rows per CTA pass (RPW x run per warp group)
   int line_run = 0;
   bool line_auto = false;  // the solver may pick it (measured winner for this (K, P))
+  // k1_stage alternative (TMA-staged blocks, kernels_stage.cuh): block height
+  // and its dynamic shared memory for (cap, wmax, stages)
+  const void* k1_stage = nullptr;
+  int stage_R = 0;
+  int (*stage_smem)(int cap, int wmax, int ns) = nullptr;
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -109,6 +119,9 @@ void fill_table(FastTable* t) {
     // B200 sweeps: k1_line wins only at K = 64, P >= 8 (C5
     // 7.42 -> 7.16 ms); at K <= 32 and K = 64, P < 8 it is 2-19% slower.
     t->line_auto = K == 64 && P >= 8;
+    t->k1_stage = (const void*)&k1_stage<K, P, W, BKG_STAGE_TPW, G>;
+    t->stage_R = StageLayout<K, P, W, BKG_STAGE_TPW>::R;
+    t->stage_smem = &k1_stage_smem<K, P, W, BKG_STAGE_TPW, G>;
   } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;

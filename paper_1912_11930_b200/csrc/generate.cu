@@ -217,7 +217,13 @@ void dev_generate_stencil_rows(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int
 }
 
 int64_t stencil_rows_nnz(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1) {
-  if (kind == 4) return first_entry_27pt(nx, ny, nz, r1) - first_entry_27pt(nx, ny, nz, r0);
+  if (kind == 4) {  // first_entry_27pt holds for r < n; r == n: all (3nx-2)(3ny-2)(3nz-2)
+    auto at = [&](int64_t r) {
+      return r < nx * ny * nz ? first_entry_27pt(nx, ny, nz, r)
+                              : (3 * nx - 2) * (3 * ny - 2) * (3 * nz - 2);
+    };
+    return at(r1) - at(r0);
+  }
   const int64_t z = kind == 3 ? nz : 1;
   auto at = [&](int64_t r) {  // entries before row r; r == n: all of them
     const int64_t n = nx * ny * z;

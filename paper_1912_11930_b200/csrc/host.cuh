@@ -21,6 +21,8 @@ void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, d
 void dev_generate_stencil_rows(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
                                uint64_t seed, double contrast, int64_t r0, int64_t r1,
                                int64_t cshift, int64_t* rowptr, int32_t* cols, double* vals);
+bool stage_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                 const double* vals, int R, int max_segs, StageCsr& out);
 int64_t stencil_rows_nnz(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1);
 void dev_generate_stencil(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
                           uint64_t seed, double contrast, bkg_matrix* m);

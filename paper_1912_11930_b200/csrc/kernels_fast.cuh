@@ -198,6 +198,20 @@ struct IterArgs {
   // launch X += Pold lambda_old + P lambda (lambda_old at coef + 4 cs).
   double* Pn;
   const double* Pold;
+  // k1_stage (kernels_stage.cuh): the staged-block copy (common.cuh
+  // StageCsr), the ring depth, and the blocks of this launch --
+  // [stg_first1, +stg_cnt1) then [stg_first2, +stg_cnt2) (the partitioned
+  // solver launches interior and boundary blocks separately).
+  const int64_t* stg_bseg;
+  const int64_t* stg_bent;
+  const int2* stg_segs;
+  const double* stg_vals;
+  const uint16_t* stg_lidx;
+  const int32_t* stg_own;
+  int stg_nstage, stg_cap, stg_wmax;
+  int64_t stg_first1, stg_cnt1, stg_first2, stg_cnt2;
+  // dist: add this launch's alpha to red1 instead of overwriting it
+  int dist_acc;
 };
 
 // Last-CTA epilogue shared by both numerics modes: norms[k] are the column

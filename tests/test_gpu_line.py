@@ -19,9 +19,11 @@ SHAPES = [(8, 8, False), (8, 4, True), (16, 16, False), (16, 4, True), (32, 8, F
           (32, 1, False), (64, 16, False), (64, 4, True), (64, 1, False), (4, 2, False)]
 
 
-@pytest.fixture(params=["1", "0"], ids=["line", "wide"])
+@pytest.fixture(params=["line", "wide", "stage"])
 def k1_choice(request, monkeypatch):
-    monkeypatch.setenv("BKG_K1_LINE", request.param)
+    """Force one K1: k1_line, k1_wide, or k1_stage (TMA-staged blocks)."""
+    monkeypatch.setenv("BKG_K1_LINE", "1" if request.param == "line" else "0")
+    monkeypatch.setenv("BKG_K1_STAGE", "1" if request.param == "stage" else "0")
     return request.param
 
 
@@ -85,6 +87,7 @@ def test_line_solve_meets_parity_bars(port, monkeypatch, k, p, glob):
     DESIGN.md §2), so the literal bars apply: history 1e-9 relative per
     iteration, iterations +-1, X 1e-8."""
     monkeypatch.setenv("BKG_K1_LINE", "1")
+    monkeypatch.setenv("BKG_K1_STAGE", "0")
     a = bk.stencil(3, 40, 36, 29, seed=11)
     n = a.n()
     b = bk.normal_block_rhs(n, k, 7)
@@ -104,27 +107,32 @@ def test_line_solve_meets_parity_bars(port, monkeypatch, k, p, glob):
 
 
 def test_line_and_wide_agree_on_large_system(monkeypatch):
-    """At a shape where the solver picks k1_line by itself (3D 7-point 96^3,
-    k = 64, p = 16: the C5 kernel table),
-    a fixed-iteration solve with k1_line forced on and off: the two K1s sum a
-    row's products in different orders only."""
+    """At the C5 kernel table (3D 7-point 96^3, k = 64, p = 16), a
+    fixed-iteration solve with the solver's own choice (k1_stage), k1_line
+    and k1_wide: the K1s sum a row's products in different orders only."""
     a = bk.stencil(3, 96, 96, 96, seed=11)
     n = a.n()
     b = bk.normal_block_rhs(n, 64, 7)
     cfg = bk.SubalgebraConfig(64, 16, "hybrid")
     opts = bk.SolveOptions(tol=1e-300, max_iter=40, record_history=True)
     out = {}
-    for v in ("auto", "1", "0"):
-        if v == "auto":
-            monkeypatch.delenv("BKG_K1_LINE", raising=False)
-        else:
+    kernels = {}
+    for v in ("auto", "1", "0", "stage"):
+        monkeypatch.delenv("BKG_K1_LINE", raising=False)
+        monkeypatch.delenv("BKG_K1_STAGE", raising=False)
+        if v in ("1", "0"):
             monkeypatch.setenv("BKG_K1_LINE", v)
+            monkeypatch.setenv("BKG_K1_STAGE", "0")
+        elif v == "stage":
+            monkeypatch.setenv("BKG_K1_STAGE", "1")
         ctx = bk.Context(0, "fast")
         res = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), cfg, opts, ctx=ctx)
         out[v] = (res.x, np.array(res.report.defect_history))
+        kernels[v] = ctx.last_k1()
         ctx.close()
-    for v in ("auto", "0"):
+    assert kernels == {"auto": "k1_stage", "1": "k1_line", "0": "k1_wide", "stage": "k1_stage"}
+    for v in ("auto", "0", "stage"):
         assert _drift(out[v][1], out["1"][1]) <= 1e-9
         xr = np.linalg.norm(out[v][0] - out["1"][0], axis=0) / np.linalg.norm(out["1"][0], axis=0)
         assert np.max(xr) <= 1e-9, xr
-    assert out["auto"][0].tobytes() == out["1"][0].tobytes()  # auto picks k1_line here
+    assert out["auto"][0].tobytes() == out["stage"][0].tobytes()  # auto picks k1_stage here
