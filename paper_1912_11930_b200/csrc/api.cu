@@ -511,7 +511,7 @@ __global__ void k_ilu_finish(Ctrl* ctrl, int nblk, int p, int k, double* coef, i
 // 27-point row, where the window saves too little) and the system is large
 // enough for every resident warp to get >= 2 super tiles of runs.
 // BKG_K1_LINE=0/1 forces it off/on (sweeps, tests).
-bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
+bool bkg::use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
   if (!ft.k1_line || A->n == 0) return false;
   const char* env = std::getenv("BKG_K1_LINE");
   if (env && env[0] == '0') return false;
@@ -546,7 +546,7 @@ bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
 // the ring takes as many stages (2..BKG_STAGE_NS, default 6) as fit the
 // shared memory of BKG_STAGE_CTAS (default 1) CTAs per SM.
 // BKG_K1_STAGE=0 turns it off (register-gather K1s).  *ns / *smem out.
-bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem) {
+bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem) {
   if (!ft.k1_stage || A->n == 0) return false;
   const char* env = std::getenv("BKG_K1_STAGE");
   if (env && env[0] == '0') return false;

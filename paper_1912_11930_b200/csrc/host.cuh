@@ -15,6 +15,9 @@ void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void**
 void allow_smem(const void* fn, int bytes);
 int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
+// per-matrix K1 choices (api.cu): k1_stage (ring depth, smem out), k1_line
+bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem);
+bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft);
 // generate.cu: device-side problem generation
 void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
                       int64_t row0 = 0);

@@ -210,6 +210,7 @@ struct IterArgs {
   const int32_t* stg_own;
   int stg_nstage, stg_cap, stg_wmax;
   int64_t stg_first1, stg_cnt1, stg_first2, stg_cnt2;
+  const int64_t* stg_map;  // non-null: block j of the launch is stg_map[j]
   // dist: add this launch's alpha to red1 instead of overwriting it
   int dist_acc;
 };

@@ -119,9 +119,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
                                              (size_t)wmax * R * 8);
   };
 
-  // blocks of this launch: [first1, first1 + cnt1) then [first2, first2 + cnt2)
+  // blocks of this launch: [first1, first1 + cnt1) then [first2, first2 + cnt2),
+  // or stg_map[0 .. cnt1 + cnt2) (the partitioned solver's interior / boundary)
   const int64_t ntot = a.stg_cnt1 + a.stg_cnt2;
   auto block_of = [&](int64_t j) {
+    if (a.stg_map) return __ldg(a.stg_map + j);
     return j < a.stg_cnt1 ? a.stg_first1 + j : a.stg_first2 + (j - a.stg_cnt1);
   };
   const int64_t nmine =
@@ -261,13 +263,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
         const int tr = 4 * cc + (lane & 3);
         const int64_t prow = r0 + tile * RPW + tr;
         const double* pr = rows + (own + tile * RPW + tr) * K + cs * W + (lane >> 2);
-        const double* qr = scr + tr * SS + (lane >> 2);
+        const double* qr = scr + tr * SS;
 #pragma unroll
         for (int pi = 0; pi < L::NPAIR; ++pi) {
           int at, bt;
           wide_pair<K, P, W, 4>(pi, at, bt);
           const double av = prow < a.n ? pr[at * 8] : 0.0;
-          const int qc = bt * 8;
+          const int qc = bt * 8 + (lane >> 2);  // logical column -> scratch column
           const double bv = qr[qc < W / 2 ? qc : qc + 2];
           double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
           dmma(d, av, bv);

@@ -24,6 +24,11 @@
 #include "host.cuh"
 #include "kernels_fast.cuh"
 
+// Deferred X update in the partitioned loop (P ping-pong, as api.cu).
+#ifndef BKG_PSOLVER_DEFER_X
+#define BKG_PSOLVER_DEFER_X 1
+#endif
+
 namespace bkg {
 
 // ------------------------------------------------------------- NCCL ---
@@ -165,16 +170,36 @@ struct Part {
   int64_t r0 = 0, r1 = 0, nloc = 0;  // owned global rows [r0, r1)
   int64_t lo = 0, hi = 0;            // extended operand rows [lo, hi) (lo <= r0, hi >= r1)
   int64_t nnz = 0;
-  DevBuf<int64_t> rowptr;
-  DevBuf<int32_t> cols;  // local columns: global - r0 (negative for ghost rows below)
-  DevBuf<double> vals;
-  SellCsr sell;          // sliced-ELL copy for k1_wide (built at setup)
-  DevBuf<double> B, X, R, Q, Pext, coef, limits, hist, red1, red2, partials, gpart, tmp;
+  // local CSR (columns: global - r0, negative for ghost rows below) with its
+  // lazily built K1 copies (sliced ELL / staged blocks); ctx stays null
+  bkg_matrix A;
+  DevBuf<double> B, X, R, Q, coef, limits, hist, red1, red2, partials, gpart, tmp;
+  DevBuf<double> Pext[2];  // P ping-pong (deferred X), each with its ghost rows
+  double* P[2] = {nullptr, nullptr};  // own rows inside Pext[i]
   DevBuf<char> ctrl_buf;
-  double* P = nullptr;  // own rows inside Pext
-  int g1 = 1, g2 = 1, g3 = 1;
+  // K1 of this part: 2 k1_stage (interior / boundary block lists), 1 k1_line,
+  // 0 k1_wide
+  int k1_kind = 0, k1_run = 0, stage_ns = 0, smem_k1 = 0;
+  const void* k1 = nullptr;
+  DevBuf<int64_t> map_in, map_bd;  // k1_stage blocks without / with ghost rows
+  int64_t nin = 0, nbd = 0;
+  int g1 = 1, g1i = 1, g1b = 1, g2 = 1, g3 = 1;
   Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_buf.ptr); }
 };
+
+// 1 for staged blocks that read a ghost row (a segment outside [0, nloc)).
+__global__ void k_block_ghost(int64_t nblk, int64_t nloc, const int64_t* __restrict__ bseg,
+                              const int2* __restrict__ segs, unsigned char* __restrict__ flag) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    unsigned char f = 0;
+    for (int64_t i = bseg[b]; i < bseg[b + 1]; ++i) {
+      const int2 sg = segs[i];
+      if (sg.x < 0 || (int64_t)sg.x + sg.y > nloc) f = 1;
+    }
+    flag[b] = f;
+  }
+}
 
 }  // namespace bkg
 
@@ -201,10 +226,18 @@ struct bkg_psolver {
   std::vector<double> history;
   uint64_t history_rows = 0;
   bool have_b = false;
+  bool defer = BKG_PSOLVER_DEFER_X;  // deferred X update, P ping-pong (api.cu k3_for)
+  uint64_t iter_launched = 0;
+  // halo on a side stream, overlapped with the interior blocks of K1
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_p = nullptr, ev_h = nullptr;
 
   ~bkg_psolver() {
     if (h_ctrl) cudaFreeHost(h_ctrl);
     if (h_ring) cudaFreeHost(h_ring);
+    if (ev_p) cudaEventDestroy(ev_p);
+    if (ev_h) cudaEventDestroy(ev_h);
+    if (hstream) cudaStreamDestroy(hstream);
     if (comm) nccl().CommDestroy(comm);
   }
 
@@ -228,12 +261,14 @@ struct bkg_psolver {
     }
     pt.lo = mn;
     pt.hi = mx;
-    pt.rowptr.alloc(pt.nloc + 1);
-    pt.cols.alloc(lc.size());
-    pt.vals.alloc(std::max<uint64_t>(nnz, 1));
-    h2d(ctx, reinterpret_cast<uint64_t*>(pt.rowptr.ptr), lrowptr, pt.nloc + 1);
-    h2d(ctx, pt.cols.ptr, lc.data(), nnz);
-    h2d(ctx, pt.vals.ptr, vals, nnz);
+    pt.A.n = (uint64_t)pt.nloc;
+    pt.A.nnz = nnz;
+    pt.A.rowptr.alloc(pt.nloc + 1);
+    pt.A.cols.alloc(lc.size());
+    pt.A.vals.alloc(std::max<uint64_t>(nnz, 1));
+    h2d(ctx, reinterpret_cast<uint64_t*>(pt.A.rowptr.ptr), lrowptr, pt.nloc + 1);
+    h2d(ctx, pt.A.cols.ptr, lc.data(), nnz);
+    h2d(ctx, pt.A.vals.ptr, vals, nnz);
     sync(ctx);
     parts.push_back(std::move(pt));
   }
@@ -247,16 +282,18 @@ struct bkg_psolver {
     pt.r1 = r1;
     pt.nloc = r1 - r0;
     pt.nnz = stencil_rows_nnz(kind, nx, ny, nz, r0, r1);
-    pt.rowptr.alloc(pt.nloc + 1);
-    pt.cols.alloc(std::max<int64_t>(pt.nnz, 1));
-    pt.vals.alloc(std::max<int64_t>(pt.nnz, 1));
-    dev_generate_stencil_rows(ctx, kind, nx, ny, nz, seed, contrast, r0, r1, r0, pt.rowptr.ptr,
-                              pt.cols.ptr, pt.vals.ptr);
+    pt.A.n = (uint64_t)pt.nloc;
+    pt.A.nnz = (uint64_t)pt.nnz;
+    pt.A.rowptr.alloc(pt.nloc + 1);
+    pt.A.cols.alloc(std::max<int64_t>(pt.nnz, 1));
+    pt.A.vals.alloc(std::max<int64_t>(pt.nnz, 1));
+    dev_generate_stencil_rows(ctx, kind, nx, ny, nz, seed, contrast, r0, r1, r0,
+                              pt.A.rowptr.ptr, pt.A.cols.ptr, pt.A.vals.ptr);
     DevBuf<int> mm(2);
     const int init[2] = {0x7fffffff, (int)0x80000000};
     h2d(ctx, mm.ptr, init, 2);
     int64_t nz_ = pt.nnz;
-    const int32_t* cp = pt.cols.ptr;
+    const int32_t* cp = pt.A.cols.ptr;
     int* mp = mm.ptr;
     void* args[] = {&nz_, &cp, &mp};
     launch(ctx, (const void*)&k_col_range, elem_grid(ctx, pt.nnz), 256, 0, args);
@@ -266,6 +303,66 @@ struct bkg_psolver {
     pt.lo = std::min(r0, r0 + (int64_t)h[0]);
     pt.hi = std::max(r1, r0 + (int64_t)h[1] + 1);
     parts.push_back(std::move(pt));
+  }
+
+  // K1 of a part: k1_stage with its blocks split into those that read ghost
+  // rows (boundary: launched after the halo) and the rest (interior:
+  // launched while the halo is in flight); else k1_line / k1_wide after the
+  // halo.  BKG_HALO_SMS (default 4 with NCCL) SMs are left to NCCL's kernels
+  // during the interior launch.
+  void choose_k1(Part& pt) {
+    FastTable base;
+    use_fast(ctx, k, p, global, &base);
+    pt.k1 = base.k1;
+    pt.smem_k1 = base.smem_k1;
+    pt.k1_kind = 0;
+    pt.k1_run = 0;
+    int rpc = base.rpc_k1;
+    if (use_stage(ctx, &pt.A, ft, &pt.stage_ns, &pt.smem_k1)) {
+      pt.k1_kind = 2;
+      pt.k1 = ft.k1_stage;
+      const StageCsr& st = pt.A.stage;
+      DevBuf<unsigned char> flag(std::max<int64_t>(st.nblk, 1));
+      int64_t nb = st.nblk, nl = pt.nloc;
+      const int64_t* bs = st.bseg.ptr;
+      const int2* sg = st.segs.ptr;
+      unsigned char* fp = flag.ptr;
+      void* args[] = {&nb, &nl, &bs, &sg, &fp};
+      launch(ctx, (const void*)&k_block_ghost, elem_grid(ctx, nb), 256, 0, args);
+      std::vector<unsigned char> hf(st.nblk);
+      d2h(ctx, hf.data(), flag.ptr, st.nblk);
+      sync(ctx);
+      std::vector<int64_t> in, bd;
+      for (int64_t b = 0; b < st.nblk; ++b) (hf[b] ? bd : in).push_back(b);
+      pt.nin = (int64_t)in.size();
+      pt.nbd = (int64_t)bd.size();
+      pt.map_in.alloc(std::max<int64_t>(pt.nin, 1));
+      pt.map_bd.alloc(std::max<int64_t>(pt.nbd, 1));
+      h2d(ctx, pt.map_in.ptr, in.data(), in.size());
+      h2d(ctx, pt.map_bd.ptr, bd.data(), bd.size());
+      int occ = 1;
+      allow_smem(pt.k1, pt.smem_k1);
+      BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt.k1, kThreads,
+                                                                   pt.smem_k1));
+      occ = std::max(occ, 1);
+      const char* hs = std::getenv("BKG_HALO_SMS");
+      const int reserve = use_nccl && nranks > 1 ? (hs ? std::atoi(hs) : 4) : 0;
+      const int full = occ * ctx->sm_count;
+      pt.g1i = (int)std::max<int64_t>(1, std::min<int64_t>(full - occ * reserve, pt.nin));
+      pt.g1b = (int)std::max<int64_t>(1, std::min<int64_t>(full, pt.nbd));
+      pt.g1 = std::max(pt.g1i, pt.g1b);
+      return;
+    }
+    if (use_line(ctx, &pt.A, ft)) {
+      pt.k1_kind = 1;
+      pt.k1 = ft.k1_line;
+      pt.k1_run = ft.line_run;
+      rpc = ft.rpc_k1_line;
+    }
+    if (ft.sell_rows)
+      sell_build(ctx, pt.nloc, pt.A.rowptr.ptr, pt.A.cols.ptr, pt.A.vals.ptr, ft.sell_rows,
+                 pt.A.sell, nullptr, pt.k1_run);
+    pt.g1 = occupancy_grid(ctx, pt.k1, pt.smem_k1, pt.nloc, rpc);
   }
 
   void finish_setup() {
@@ -280,9 +377,11 @@ struct bkg_psolver {
       pt.X.alloc(nk);
       pt.R.alloc(nk);
       pt.Q.alloc(nk);
-      pt.Pext.alloc((size_t)(pt.hi - pt.lo) * k);
-      BKG_CUDA_CHECK(cudaMemsetAsync(pt.Pext.ptr, 0, pt.Pext.bytes(), ctx->stream));
-      pt.P = pt.Pext.ptr + (size_t)(pt.r0 - pt.lo) * k;
+      for (int i = 0; i < (defer ? 2 : 1); ++i) {
+        pt.Pext[i].alloc((size_t)(pt.hi - pt.lo) * k);
+        BKG_CUDA_CHECK(cudaMemsetAsync(pt.Pext[i].ptr, 0, pt.Pext[i].bytes(), ctx->stream));
+        pt.P[i] = pt.Pext[i].ptr + (size_t)(pt.r0 - pt.lo) * k;
+      }
       pt.coef.alloc((size_t)6 * cs);
       pt.limits.alloc(k);
       pt.hist.alloc((size_t)ring * k);
@@ -291,14 +390,13 @@ struct bkg_psolver {
       pt.tmp.alloc((size_t)cs + k);
       pt.ctrl_buf.alloc(sizeof(Ctrl));
       BKG_CUDA_CHECK(cudaMemsetAsync(pt.ctrl_buf.ptr, 0, sizeof(Ctrl), ctx->stream));
-      pt.g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, pt.nloc, ft.rpc_k1);
+      choose_k1(pt);
       pt.g2 = occupancy_grid(ctx, ft.k2, ft.smem_iter, pt.nloc, ft.rpc_k2);
-      pt.g3 = occupancy_grid(ctx, ft.k3, ft.smem_iter, pt.nloc, ft.rpc_k3);
+      pt.g3 = std::min(occupancy_grid(ctx, ft.k3x[0][1], ft.smem_iter, pt.nloc, ft.rpc_k3),
+                       occupancy_grid(ctx, ft.k3x[0][2], ft.smem_iter, pt.nloc, ft.rpc_k3));
       const int gmax = std::max(std::max(pt.g1, pt.g2), pt.g3);
       pt.partials.alloc((size_t)gmax * ft.e_iter);
       pt.gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
-      if (ft.sell_rows)
-        sell_build(ctx, pt.nloc, pt.rowptr.ptr, pt.cols.ptr, pt.vals.ptr, ft.sell_rows, pt.sell);
     }
     if (!use_nccl) {
       std::vector<double*> r1, r2, t;
@@ -314,21 +412,27 @@ struct bkg_psolver {
       h2d(ctx, red2_ptrs.ptr, r2.data(), r2.size());
       h2d(ctx, tmp_ptrs.ptr, t.data(), t.size());
     }
+    BKG_CUDA_CHECK(cudaStreamCreateWithFlags(&hstream, cudaStreamNonBlocking));
+    BKG_CUDA_CHECK(cudaEventCreateWithFlags(&ev_p, cudaEventDisableTiming));
+    BKG_CUDA_CHECK(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl), cudaHostAllocDefault));
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     sync(ctx);
   }
 
   // -- communication -----------------------------------------------------
-  // Copy the owned rows of `own(part)` into the ghost rows of `ext(part)`.
-  template <class Own, class Ext>
-  void halo(Own own, Ext ext) {
+  // Copy the owned rows of P[buf] of every part into the ghost rows of the
+  // parts that read them, on stream `st` (virtual: device copies; NCCL:
+  // grouped send/recv of contiguous row blocks over NVLink).
+  void halo(int buf, cudaStream_t st) {
     if (!use_nccl) {
       for (const HaloCopy& h : plan) {
         Part& d = parts[h.dst];
         Part& s = parts[h.src];
-        d2d(ctx, ext(d) + (size_t)(h.row - d.lo) * k, own(s) + (size_t)(h.row - s.r0) * k,
-            (size_t)h.count * k);
+        BKG_CUDA_CHECK(cudaMemcpyAsync(d.Pext[buf].ptr + (size_t)(h.row - d.lo) * k,
+                                       s.P[buf] + (size_t)(h.row - s.r0) * k,
+                                       (size_t)h.count * k * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
       }
       return;
     }
@@ -337,17 +441,13 @@ struct bkg_psolver {
     BKG_NCCL_CHECK(nccl().GroupStart());
     for (const HaloCopy& h : plan) {
       if (h.src == rank)
-        BKG_NCCL_CHECK(nccl().Send(own(me) + (size_t)(h.row - me.r0) * k, (size_t)h.count * k,
-                                   ncclDouble, h.dst, comm, ctx->stream));
+        BKG_NCCL_CHECK(nccl().Send(me.P[buf] + (size_t)(h.row - me.r0) * k, (size_t)h.count * k,
+                                   ncclDouble, h.dst, comm, st));
       if (h.dst == rank)
-        BKG_NCCL_CHECK(nccl().Recv(ext(me) + (size_t)(h.row - me.lo) * k, (size_t)h.count * k,
-                                   ncclDouble, h.src, comm, ctx->stream));
+        BKG_NCCL_CHECK(nccl().Recv(me.Pext[buf].ptr + (size_t)(h.row - me.lo) * k,
+                                   (size_t)h.count * k, ncclDouble, h.src, comm, st));
     }
     BKG_NCCL_CHECK(nccl().GroupEnd());
-  }
-
-  void halo_p() {
-    halo([](Part& q) { return q.P; }, [](Part& q) { return q.Pext.ptr; });
   }
 
   // Sum a per-part vector across parts; every part gets the total.
@@ -364,15 +464,16 @@ struct bkg_psolver {
            0, args);
   }
 
-  IterArgs args_of(Part& pt, bool with_hist) {
+  IterArgs args_of(Part& pt, bool with_hist, int cur) {
     IterArgs a{};
     a.n = pt.nloc;
-    a.rowptr = pt.rowptr.ptr;
-    a.cols = pt.cols.ptr;
-    a.vals = pt.vals.ptr;
+    a.rowptr = pt.A.rowptr.ptr;
+    a.cols = pt.A.cols.ptr;
+    a.vals = pt.A.vals.ptr;
     a.X = pt.X.ptr;
     a.R = pt.R.ptr;
-    a.P = pt.P;
+    a.P = pt.P[cur];
+    a.Pn = pt.P[cur];
     a.Q = pt.Q.ptr;
     a.partials = pt.partials.ptr;
     a.gpart = pt.gpart.ptr;
@@ -385,18 +486,57 @@ struct bkg_psolver {
     a.dist = 1;
     a.red1 = pt.red1.ptr;
     a.red2 = pt.red2.ptr;
-    a.sptr = pt.sell.sptr.ptr;
-    a.scols = pt.sell.cols.ptr;
-    a.svals = pt.sell.vals.ptr;
+    a.sptr = pt.A.sell.sptr.ptr;
+    a.scols = pt.A.sell.cols.ptr;
+    a.svals = pt.A.sell.vals.ptr;
+    a.stri = pt.k1_run ? pt.A.sell.tri.ptr : nullptr;
+    if (pt.k1_kind == 2) {
+      const StageCsr& st = pt.A.stage;
+      a.stg_bseg = st.bseg.ptr;
+      a.stg_bent = st.bent.ptr;
+      a.stg_segs = st.segs.ptr;
+      a.stg_vals = st.vals.ptr;
+      a.stg_lidx = st.lidx.ptr;
+      a.stg_own = st.own.ptr;
+      a.stg_nstage = pt.stage_ns;
+      a.stg_cap = st.cap;
+      a.stg_wmax = st.wmax;
+    }
     return a;
   }
 
+  // K1 of part pt over its interior (interior = true) or boundary blocks
+  // (k1_stage), or the whole K1 (interior = false, other kernels).
+  void launch_k1(Part& pt, IterArgs a, bool interior, bool acc) {
+    a.dist_acc = acc ? 1 : 0;
+    int grid = pt.g1;
+    if (pt.k1_kind == 2) {
+      a.stg_map = interior ? pt.map_in.ptr : pt.map_bd.ptr;
+      a.stg_cnt1 = interior ? pt.nin : pt.nbd;
+      grid = interior ? pt.g1i : pt.g1b;
+    }
+    void* args[] = {&a};
+    launch(ctx, pt.k1, grid, kThreads, pt.smem_k1, args);
+  }
+
   void iteration(bool with_hist) {
-    halo_p();
+    const bool odd = defer && (iter_launched++ & 1) != 0;
+    const int cur = odd ? 1 : 0;
+    // halo of P[cur] on the side stream once the previous K3 wrote it
+    BKG_CUDA_CHECK(cudaEventRecord(ev_p, ctx->stream));
+    BKG_CUDA_CHECK(cudaStreamWaitEvent(hstream, ev_p, 0));
+    halo(cur, hstream);
+    BKG_CUDA_CHECK(cudaEventRecord(ev_h, hstream));
+    // K1 interior blocks overlap the halo; boundary blocks (and the other
+    // K1 kernels) after it
+    for (Part& pt : parts)
+      if (pt.k1_kind == 2 && pt.nin > 0) launch_k1(pt, args_of(pt, with_hist, cur), true, false);
+    BKG_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_h, 0));
     for (Part& pt : parts) {
-      IterArgs a = args_of(pt, with_hist);
-      void* args[] = {&a};
-      launch(ctx, ft.k1, pt.g1, kThreads, ft.smem_k1, args);
+      if (pt.k1_kind != 2)
+        launch_k1(pt, args_of(pt, with_hist, cur), false, false);
+      else if (pt.nbd > 0)
+        launch_k1(pt, args_of(pt, with_hist, cur), false, pt.nin > 0);
     }
     allreduce([](Part& q) -> DevBuf<double>& { return q.red1; }, red1_ptrs, 2 * cs);
     const int smem = (int)sizeof(double) * (bsolve_ws_doubles(p, 256) + k);
@@ -411,7 +551,7 @@ struct bkg_psolver {
       launch(ctx, (const void*)&k_dist_lambda, 1, 256, smem, args);
     }
     for (Part& pt : parts) {
-      IterArgs a = args_of(pt, with_hist);
+      IterArgs a = args_of(pt, with_hist, cur);
       void* args[] = {&a};
       launch(ctx, ft.k2, pt.g2, kThreads, ft.smem_iter, args);
     }
@@ -426,10 +566,19 @@ struct bkg_psolver {
       void* args[] = {&c, &nb, &pp, &kk, &r2, &cf, &c_s, &lm, &hs, &rg};
       launch(ctx, (const void*)&k_dist_beta, 1, 256, smem, args);
     }
+    // K3: deferred X (api.cu k3_for): even iterations read P[0] and write
+    // P' to P[1] leaving X (XM 1); odd ones read P[1], flush X with P[0]
+    // and lambda_old, write P' over P[0] (XM 2)
     for (Part& pt : parts) {
-      IterArgs a = args_of(pt, with_hist);
+      IterArgs a = args_of(pt, with_hist, cur);
+      const void* k3 = ft.k3x[0][0];
+      if (defer) {
+        a.Pn = pt.P[1 - cur];
+        a.Pold = odd ? pt.P[0] : nullptr;
+        k3 = ft.k3x[0][odd ? 2 : 1];
+      }
       void* args[] = {&a};
-      launch(ctx, ft.k3, pt.g3, kThreads, ft.smem_iter, args);
+      launch(ctx, k3, pt.g3, kThreads, ft.smem_iter, args);
     }
   }
 
@@ -473,14 +622,15 @@ struct bkg_psolver {
     h.done = conv ? 1 : 0;
     h.converged = conv ? 1 : 0;
     h.max_iter = max_iter;
+    iter_launched = 0;
     for (Part& pt : parts) {
       h2d(ctx, pt.limits.ptr, lim.data(), k);
       h2d(ctx, pt.ctrl_buf.ptr, reinterpret_cast<const char*>(&h), sizeof(Ctrl));
-      if (!conv) d2d(ctx, pt.P, pt.R.ptr, (size_t)pt.nloc * k);
+      if (!conv) d2d(ctx, pt.P[0], pt.R.ptr, (size_t)pt.nloc * k);
     }
     if (!conv) {  // rho_prev^1 = <<P^1, R^0>> (local partials; reduced after K1)
       for (Part& pt : parts)
-        dev_gram(ctx, pt.nloc, k, p, global, pt.P, pt.R.ptr, pt.red1.ptr + cs, false);
+        dev_gram(ctx, pt.nloc, k, p, global, pt.P[0], pt.R.ptr, pt.red1.ptr + cs, false);
     }
     cudaEvent_t e0, e1;
     BKG_CUDA_CHECK(cudaEventCreate(&e0));
@@ -489,7 +639,10 @@ struct bkg_psolver {
     uint64_t seen = 0;
     bool done = conv;
     while (!done) {
-      for (int i = 0; i < chunk; ++i) iteration(record);
+      // never queue iterations (and their collectives) past max_iter
+      const uint64_t left = max_iter > seen ? max_iter - seen : 1;
+      const int nq = (int)std::min<uint64_t>((uint64_t)chunk, left);
+      for (int i = 0; i < nq; ++i) iteration(record);
       d2h(ctx, reinterpret_cast<char*>(h_ctrl), parts[0].ctrl_buf.ptr, sizeof(Ctrl));
       if (record) d2h(ctx, h_ring, parts[0].hist.ptr, (size_t)ring * k);
       sync(ctx);
@@ -536,19 +689,10 @@ struct bkg_psolver {
 
   // Explicit residual ||B - A X|| per column (solver.hpp:203-207).
   std::vector<double> final_norms() {
-    for (Part& pt : parts) d2d(ctx, pt.P, pt.X.ptr, (size_t)pt.nloc * k);
-    halo_p();
+    for (Part& pt : parts) d2d(ctx, pt.P[0], pt.X.ptr, (size_t)pt.nloc * k);
+    halo(0, ctx->stream);
     for (Part& pt : parts) {
-      bkg_matrix m;  // non-owning view of the part's local CSR
-      m.n = pt.nloc;
-      m.nnz = pt.nnz;
-      m.rowptr.ptr = pt.rowptr.ptr;
-      m.cols.ptr = pt.cols.ptr;
-      m.vals.ptr = pt.vals.ptr;
-      dev_spmm(ctx, &m, k, pt.P, pt.Q.ptr, nullptr, false);
-      m.rowptr.ptr = nullptr;
-      m.cols.ptr = nullptr;
-      m.vals.ptr = nullptr;
+      dev_spmm(ctx, &pt.A, k, pt.P[0], pt.Q.ptr, nullptr, false);
       int64_t tot = pt.nloc * (int64_t)k;
       const double* b = pt.B.ptr;
       double* q = pt.Q.ptr;
