@@ -218,6 +218,11 @@ int bkg_psolver_create_nccl_generated(bkg_ctx* ctx, int kind, uint64_t nx, uint6
  * global n*k; NCCL: this rank's rows).                                      */
 int bkg_psolver_generate_rhs(bkg_psolver* s, int distribution, uint64_t seed);
 int bkg_psolver_get_rhs(bkg_psolver* s, double* b);
+/* Part `part` (virtual: 0..nparts-1; NCCL: 0 = this rank): out[0] = K1
+ * variant (bkg_solve_k1_variant codes), out[1] / out[2] = k1_stage blocks
+ * launched before / after the halo (interior / boundary), out[3] / out[4] =
+ * the part's global rows [r0, r1).                                          */
+int bkg_psolver_part_info(const bkg_psolver* s, int part, int64_t* out);
 int bkg_psolver_destroy(bkg_psolver* s);
 /* virtual: global B (n*k); NCCL: this rank's rows.                         */
 int bkg_psolver_set_rhs(bkg_psolver* s, const double* b);

@@ -123,6 +123,7 @@ SIGNATURES = [
       C.POINTER(C.c_void_p)]),
     ("bkg_psolver_generate_rhs", C.c_int, [_vp, C.c_int, C.c_uint64]),
     ("bkg_psolver_get_rhs", C.c_int, [_vp, _d]),
+    ("bkg_psolver_part_info", C.c_int, [_vp, C.c_int, C.POINTER(C.c_int64)]),
     ("bkg_psolver_destroy", C.c_int, [_vp]),
     ("bkg_psolver_set_rhs", C.c_int, [_vp, _d]),
     ("bkg_psolver_run", C.c_int, [_vp, C.c_double, C.c_uint64, C.c_int, _d, C.POINTER(Report)]),

@@ -10,6 +10,7 @@ bool fast_lookup(int k, int p, bool global, FastTable* t) {
     case 16: return fast_lookup_k<16>(p, global, t);
     case 32: return fast_lookup_k<32>(p, global, t);
     case 64: return fast_lookup_k<64>(p, global, t);
+    case 128: return fast_lookup_k<128>(p, global, t);
     default: return false;
   }
 }

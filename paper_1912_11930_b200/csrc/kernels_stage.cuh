@@ -18,9 +18,10 @@
 // CSR works the same way (worst case one segment per distinct column).
 //
 // CTA = 8 warps, persistent over the blocks (block j of the launch goes to
-// CTA j % grid).  Warp 0 lane-parallel issues the copies of block i + NS into
-// the stage freed by block i (one __syncthreads per block), with the next
-// block's segment list prefetched into registers one block ahead.  Every warp
+// CTA j % grid).  The last warp to finish block i (a shared-memory counter
+// per stage) lane-parallel issues the copies of block i + NS into the stage
+// it freed, so there is no CTA-wide barrier per block and the warps drift up
+// to NS - 1 blocks apart.  Every warp
 // computes RPW x W tiles of the staged block: lane (rr, cl) owns row rr and
 // the columns {2cl, 2cl + 1, W/2 + 2cl, W/2 + 2cl + 1} of its warp's column
 // slice, so each operand row read is two conflict-free LDS.128 per lane
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
   uint64_t* bar =
       reinterpret_cast<uint64_t*>(smraw + (size_t)NS * sbytes + (kThreads / 32) * RPW * SS * 8);
   int* hdr = reinterpret_cast<int*>(bar + NS);  // per stage: own, w
+  int* fin = hdr + 2 * NS;                      // per stage: warps done with it
   auto rows_of = [&](int s) { return reinterpret_cast<const double*>(smraw + (size_t)s * sbytes); };
   auto vals_of = [&](int s) {
     return reinterpret_cast<const double*>(smraw + (size_t)s * sbytes + (size_t)cap * K * 8);
@@ -187,7 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(bar + s, 1);
+      fin[s] = 0;
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -196,7 +201,6 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
       load_meta(i);
       issue((int)i);
     }
-    load_meta(NS);
   }
   __syncthreads();
 
@@ -279,10 +283,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
       }
       __syncwarp();
     }
-    __syncthreads();  // stage s is free
-    if (warp == 0 && i + NS < nmine) {
-      issue(s);
-      load_meta(i + NS + 1);
+    // The last warp done with stage s refills it with block i + NS: no
+    // CTA-wide barrier per block, warps drift up to NS - 1 blocks apart.
+    __threadfence_block();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(fin + s, 1) == kThreads / 32 - 1;
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      if (lane == 0) fin[s] = 0;
+      if (i + NS < nmine) {
+        load_meta(i + NS);
+        issue(s);
+      }
     }
   }
   __syncthreads();  // the stages are reused as the reduction buffer
@@ -309,7 +321,7 @@ int k1_stage_smem(int cap, int wmax, int ns) {
   using S = FastSmem<K, P, 1, GLOBAL>;
   constexpr int R = StageLayout<K, P, W, TPW>::R;
   const int main = ns * stage_bytes(K, R, cap, wmax) + (kThreads / 32) * L::RPW * L::SS * 8 +
-                   ns * 8 + ns * 8;
+                   ns * 8 + ns * 12;
   const int epi = (int)sizeof(double) * (L::RED + 3 * S::CS + bsolve_ws_doubles(P, kThreads) + K);
   return main > epi ? main : epi;
 }

@@ -370,7 +370,7 @@ struct bkg_psolver {
     nblk = global ? 1 : k / p;
     cs = nblk * p * p;
     BKG_REQUIRE(use_fast(ctx, k, p, global, &ft), BKG_CONFIG,
-                "psolver: (k, p) needs the tuned fast kernels (k in {4,8,16,32,64}, p <= 16)");
+                "psolver: (k, p) needs the tuned fast kernels (k in {4,8,16,32,64,128}, p <= 16)");
     for (Part& pt : parts) {
       const size_t nk = (size_t)pt.nloc * k;
       pt.B.alloc(nk);
@@ -896,6 +896,18 @@ int bkg_psolver_get_rhs(bkg_psolver* s, double* b) {
       d2h(s->ctx, b + (size_t)off * s->k, pt.B.ptr, (size_t)pt.nloc * s->k);
     }
     sync(s->ctx);
+  });
+}
+
+int bkg_psolver_part_info(const bkg_psolver* s, int part, int64_t* out) {
+  return pguard([&] {
+    BKG_REQUIRE(part >= 0 && part < (int)s->parts.size(), BKG_CONFIG, "psolver: no such part");
+    const Part& pt = s->parts[part];
+    out[0] = pt.k1_kind;
+    out[1] = pt.k1_kind == 2 ? pt.nin : 0;
+    out[2] = pt.k1_kind == 2 ? pt.nbd : 0;
+    out[3] = pt.r0;
+    out[4] = pt.r1;
   });
 }
 

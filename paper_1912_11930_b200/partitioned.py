@@ -153,6 +153,15 @@ class PartitionedSolver:
         _check(N.lib().bkg_psolver_history(self.handle, _dp(out), cap, C.byref(rows)))
         return out[: min(cap, rows.value)]
 
+    def part_info(self, part: int = 0) -> dict:
+        """K1 of a part and its interior / boundary block split
+        (bkg_psolver_part_info)."""
+        out = (C.c_int64 * 5)()
+        _check(N.lib().bkg_psolver_part_info(self.handle, part, out))
+        from .blockkrylov import Context
+        return {"k1": Context.K1_VARIANTS[int(out[0])], "interior_blocks": int(out[1]),
+                "boundary_blocks": int(out[2]), "rows": (int(out[3]), int(out[4]))}
+
     def close(self) -> None:
         if self.handle:
             N.lib().bkg_psolver_destroy(self.handle)

@@ -9,7 +9,9 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [(8, 8, False), (8, 4, True), (16, 16, False), (16, 4, False), (16, 4, True),
           (32, 8, False), (32, 1, False), (64, 16, False), (64, 4, True), (64, 1, False),
-          (4, 2, False), (16, 8, True)]
+          (4, 2, False), (16, 8, True),
+          # k = 128: the paper's experiment width
+          (128, 16, False), (128, 8, False), (128, 4, True), (128, 1, False)]
 
 
 @pytest.mark.parametrize("k,p,glob", SHAPES)

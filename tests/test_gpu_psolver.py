@@ -136,3 +136,42 @@ def test_nccl_generated_matches_host_csr(ctx, kind, grid, k, p):
     assert hg.tobytes() == h.history(rep1.history_rows).tobytes()
     assert xg.tobytes() == h.x().tobytes()
     h.close()
+
+
+@pytest.mark.parametrize("nparts", [2, 3])
+@pytest.mark.parametrize("stage", ["1", "0"])
+def test_interior_boundary_split(ctx, monkeypatch, nparts, stage):
+    """k1_stage in the partitioned loop: every part's blocks are split into
+    interior blocks (launched while the halo copies run on the side stream)
+    and boundary blocks (after the halo event); their alpha partials are
+    summed in a fixed order.  Bars against the unpartitioned fast solve, and
+    the split itself: a z-slab part of a 7-point stencil has boundary blocks
+    only next to its neighbours (one plane each) and no ghost reads inside."""
+    monkeypatch.setenv("BKG_K1_STAGE", stage)
+    case, a, b = inputs("c2_24")
+    cfg = bk.SubalgebraConfig(case.k, case.p, case.mode)
+    s = PartitionedSolver.virtual(a, cfg, nparts, ctx)
+    plane = 24 * 24
+    for i in range(nparts):
+        info = s.part_info(i)
+        if stage == "1":
+            assert info["k1"] == "k1_stage"
+            r0, r1 = info["rows"]
+            nb = info["interior_blocks"] + info["boundary_blocks"]
+            R = -(-(r1 - r0) // nb)  # block height
+            nbrs = (i > 0) + (i < nparts - 1)
+            assert 0 < info["boundary_blocks"] <= nbrs * (-(-plane // R) + 1)
+            assert info["interior_blocks"] > 0
+        else:
+            assert info["k1"] in ("k1_wide", "k1_line")
+    s.set_rhs(b)
+    rep, _ = s.run(1e-300, 40, record_history=True)
+    hist, x = s.history(rep.history_rows), s.x()
+    s.close()
+    ref = bk.bcg_solve(a, b, bk.Preconditioner.identity(a.n()), cfg,
+                       bk.SolveOptions(tol=1e-300, max_iter=40, record_history=True), ctx=ctx)
+    h1 = np.array(ref.report.defect_history)
+    assert rep.iterations == ref.report.iterations == 40
+    assert np.max(np.abs(hist - h1) / h1) <= 1e-9
+    xr = np.linalg.norm(x - ref.x, axis=0) / np.linalg.norm(ref.x, axis=0)
+    assert np.max(xr) <= 1e-9
