@@ -83,7 +83,17 @@ int elem_grid(const bkg_ctx* c, int64_t total) {
 }
 
 void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void** args) {
-  BKG_CUDA_CHECK(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, c->stream));
+  const cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, c->stream);
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fn);
+    throw Error(BKG_CUDA, std::string("cudaLaunchKernel: ") + cudaGetErrorString(e) + " (grid " +
+                              std::to_string(grid) + ", block " + std::to_string(block) +
+                              ", dynamic smem " + std::to_string(smem) + ", static smem " +
+                              std::to_string(fa.sharedSizeBytes) + ", max dynamic " +
+                              std::to_string(fa.maxDynamicSharedSizeBytes) + ", regs " +
+                              std::to_string(fa.numRegs) + ")");
+  }
   c->launches++;
 }
 
@@ -549,7 +559,7 @@ bool bkg::use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
 bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem) {
   if (!ft.k1_stage || A->n == 0) return false;
   const char* env = std::getenv("BKG_K1_STAGE");
-  if (env && env[0] == '0') return false;
+  if (!env || env[0] == '0') return false;  // opt-in until it beats the register-gather K1s
   const char* line = std::getenv("BKG_K1_LINE");
   if (line && line[0] == '1') return false;  // an explicit k1_line request wins
   StageCsr& st = A->stage;
@@ -584,6 +594,7 @@ bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* n
 struct bkg_solver {
   bkg_ctx* ctx = nullptr;
   const bkg_matrix* A = nullptr;
+  uint64_t A_serial = 0;  // A->serial when A was bound (addresses get reused)
   int64_t n = 0;
   int k = 0, p = 0;
   bool global = false;
@@ -641,7 +652,16 @@ struct bkg_solver {
       cudaGraph_t g;
       BKG_CUDA_CHECK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
       const uint64_t before = ctx->launches;
-      for (int i = 0; i < chunk; ++i) launch_iteration(true);
+      try {
+        for (int i = 0; i < chunk; ++i) launch_iteration(true);
+      } catch (...) {  // never leave the stream (and this thread) in capture mode
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(ctx->stream, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaGetLastError();
+        ctx->launches = before;
+        throw;
+      }
       graph_kernels = ctx->launches - before;  // kernels per replay (8 per ILU(0) iteration)
       ctx->launches = before;
       BKG_CUDA_CHECK(cudaStreamEndCapture(ctx->stream, &g));
@@ -656,6 +676,7 @@ struct bkg_solver {
             int pc = BKG_PRECOND_IDENTITY) {
     ctx = c;
     A = a;
+    A_serial = a->serial;
     n = (int64_t)a->n;
     k = kk;
     p = pp;
@@ -693,6 +714,7 @@ struct bkg_solver {
       g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, ft.rpc_k2);
       g3 = std::min(occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3),
                     occupancy_grid(c, ft.k3x[pcx][2], ft.smem_iter, n, ft.rpc_k3));
+      allow_smem(ft.k3x[pcx][1], ft.smem_iter);  // the skip launch (> 48 KB at k = 128)
       int gmax = std::max(std::max(g1, g2), g3);
       if (precond == BKG_PRECOND_ILU0) {
         g2i = occupancy_grid(c, ft.k2_ilu, ft.smem_iter, n, ft.rpc);
@@ -740,8 +762,9 @@ struct bkg_solver {
   // per-matrix choices so the kernel (and fast-mode summation order) depends
   // on the matrix solved, not on call history.
   void bind_matrix(const bkg_matrix* a) {
-    if (a == A) return;
+    if (a == A && a->serial == A_serial) return;
     A = a;
+    A_serial = a->serial;
     if (!fast) return;
     choose_k1();
     if (partials.count < (size_t)g1 * ft.e_iter) partials.alloc((size_t)g1 * ft.e_iter);

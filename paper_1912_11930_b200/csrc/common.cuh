@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <set>
 
 #include <cstdint>
@@ -185,6 +186,13 @@ struct bkg_ctx {
 
 struct bkg_matrix {
   bkg_ctx* ctx = nullptr;
+  // Unique per object: a cached solver workspace compares serials, not
+  // addresses (a destroyed matrix's address is reused by the next create).
+  uint64_t serial = next_serial();
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> counter{0};
+    return ++counter;
+  }
   uint64_t n = 0, nnz = 0;
   bkg::DevBuf<int64_t> rowptr;
   bkg::DevBuf<int32_t> cols;

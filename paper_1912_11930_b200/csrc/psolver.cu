@@ -394,6 +394,7 @@ struct bkg_psolver {
       pt.g2 = occupancy_grid(ctx, ft.k2, ft.smem_iter, pt.nloc, ft.rpc_k2);
       pt.g3 = std::min(occupancy_grid(ctx, ft.k3x[0][1], ft.smem_iter, pt.nloc, ft.rpc_k3),
                        occupancy_grid(ctx, ft.k3x[0][2], ft.smem_iter, pt.nloc, ft.rpc_k3));
+      allow_smem(ft.k3x[0][0], ft.smem_iter);  // observer path (no deferral)
       const int gmax = std::max(std::max(pt.g1, pt.g2), pt.g3);
       pt.partials.alloc((size_t)gmax * ft.e_iter);
       pt.gpart.alloc((size_t)kMaxTicketGroups * ft.e_iter);
