@@ -221,7 +221,8 @@ int bkg_psolver_get_rhs(bkg_psolver* s, double* b);
 /* Part `part` (virtual: 0..nparts-1; NCCL: 0 = this rank): out[0] = K1
  * variant (bkg_solve_k1_variant codes), out[1] / out[2] = k1_stage blocks
  * launched before / after the halo (interior / boundary), out[3] / out[4] =
- * the part's global rows [r0, r1).                                          */
+ * the part's global rows [r0, r1), out[5] = row slots per k1_stage block,
+ * out[6..8] = its grid box bx, by, bz (0: consecutive rows).  out: 9 values. */
 int bkg_psolver_part_info(const bkg_psolver* s, int part, int64_t* out);
 int bkg_psolver_destroy(bkg_psolver* s);
 /* virtual: global B (n*k); NCCL: this rank's rows.                         */

@@ -552,42 +552,135 @@ bool bkg::use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft) {
 }
 
 // K1 = k1_stage (TMA-staged blocks, kernels_stage.cuh) when the matrix's
-// blocks fit: the staged-block copy is built once per matrix (stage.cu) and
-// the ring takes as many stages (2..BKG_STAGE_NS, default 6) as fit the
-// shared memory of BKG_STAGE_CTAS (default 1) CTAs per SM.
-// BKG_K1_STAGE=0 turns it off (register-gather K1s).  *ns / *smem out.
-bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem) {
+// blocks fit: the staged-block copy is built once per matrix and K (stage.cu)
+// and the ring takes as many stages (2..BKG_STAGE_NS, default 6) as fit the
+// shared memory of one CTA per SM.  Block shape: on a detected grid stencil
+// the largest box from a preference list whose estimated stage (box + halo
+// shell, from the sampled column offsets) leaves room for BKG_STAGE_MINNS
+// (default 3) stages; BKG_STAGE_BOX=bx,by,bz forces one, BKG_STAGE_BOX=0
+// forces R0 x BKG_STAGE_TPW consecutive rows (also the fallback for matrices
+// without a grid).  BKG_K1_STAGE=0/1 forces it off/on.  *ns / *smem out.
+namespace {
+
+// Staged rows of an interior box: |box (+) (offsets U {0})| on the grid.
+int box_staged_rows(const int box[3], const int64_t grid[3], const std::vector<int64_t>& offs) {
+  const int64_t nx = grid[0], ny = grid[1];
+  std::set<int64_t> pts;
+  // a box far from the faces: base (nx/2, ny/2, nz/2), coordinates unclamped
+  for (int z = 0; z < box[2]; ++z)
+    for (int y = 0; y < box[1]; ++y)
+      for (int x = 0; x < box[0]; ++x) {
+        const int64_t r = ((int64_t)z * ny + y) * nx + x;
+        pts.insert(r);
+        for (int64_t d : offs) pts.insert(r + d);
+      }
+  return (int)pts.size();
+}
+
+int stage_ring_fit(const FastTable& ft, int R, int cap, int wmax, int per_cta, int nsmax) {
+  for (int q = nsmax; q >= 2; --q)
+    if (ft.stage_smem(R, cap, wmax, q) <= per_cta) return q;
+  return 0;
+}
+
+}  // namespace
+
+bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, int* ns,
+                    int* smem) {
   if (!ft.k1_stage || A->n == 0) return false;
   const char* env = std::getenv("BKG_K1_STAGE");
-  if (!env || env[0] == '0') return false;  // opt-in until it beats the register-gather K1s
+  if (env && env[0] == '0') return false;
+  if (!env && !ft.stage_auto) return false;
   const char* line = std::getenv("BKG_K1_LINE");
   if (line && line[0] == '1') return false;  // an explicit k1_line request wins
   StageCsr& st = A->stage;
-  if (st.failed_R == ft.stage_R && st.failed_n == (int64_t)A->n) return false;
-  if (st.R != ft.stage_R || st.n != (int64_t)A->n) {
-    if (!stage_build(c, (int64_t)A->n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, ft.stage_R,
-                     32 * kStageSegLanes, st)) {
-      st.failed_R = ft.stage_R;
-      st.failed_n = (int64_t)A->n;
-      return false;
-    }
-  }
+  const int64_t n = (int64_t)A->n;
+  const int R0 = ft.stage_R0;
   int optin = 0;
   BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
-  const char* ec = std::getenv("BKG_STAGE_CTAS");
-  const int ctas = ec ? std::max(1, std::atoi(ec)) : 1;
-  const int per_cta = std::min(optin, (228 * 1024) / ctas - 1024);
+  const int per_cta = std::min(optin, 227 * 1024);
   const char* en = std::getenv("BKG_STAGE_NS");
   const int nsmax = en ? std::max(2, std::atoi(en)) : 6;
-  for (int q = nsmax; q >= 2; --q) {
-    const int b = ft.stage_smem(st.cap, st.wmax, q);
-    if (b <= per_cta) {
-      *ns = q;
-      *smem = b;
-      return true;
+  const char* em = std::getenv("BKG_STAGE_MINNS");
+  const int minns = em ? std::max(2, std::atoi(em)) : 3;
+  if (st.failed_R == R0 && st.failed_n == n && st.failed_K == K) return false;
+  if (st.R == 0 || st.n != n || st.K != K || st.R % R0 != 0) {
+    if (!st.grid_checked || st.grid_n != n) {
+      st.offs.clear();
+      st.has_grid = grid_detect(c, n, A->rowptr.ptr, A->cols.ptr, st.grid_found, &st.offs);
+      st.grid_checked = true;
+      st.grid_n = n;
     }
+    int box[3] = {0, 0, 0};
+    const char* eb = std::getenv("BKG_STAGE_BOX");
+    bool forced = false;
+    if (eb) {
+      int b0 = 0, b1 = 1, b2 = 1;
+      const int got = std::sscanf(eb, "%d,%d,%d", &b0, &b1, &b2);
+      forced = true;
+      if (got >= 1 && b0 > 0 && st.has_grid) {
+        box[0] = b0;
+        box[1] = got >= 2 ? b1 : 1;
+        box[2] = got >= 3 ? b2 : 1;
+      }
+    }
+    if (!forced && st.has_grid) {
+      static const int cand3[][3] = {{8, 8, 4}, {8, 4, 4}, {4, 4, 4}, {8, 4, 2}, {4, 4, 2},
+                                     {4, 2, 2}, {8, 2, 1}, {8, 1, 1}};
+      static const int cand2[][3] = {{32, 8, 1}, {32, 4, 1}, {16, 4, 1}, {16, 2, 1},
+                                     {8, 2, 1},  {16, 1, 1}, {8, 1, 1}};
+      const bool d3 = st.grid_found[2] > 1;
+      const int(*cand)[3] = d3 ? cand3 : cand2;
+      const int nc = d3 ? 8 : 7;
+      int wguess = (int)st.offs.size() + 1;
+      for (int pass = 0; pass < 2 && box[0] == 0; ++pass)  // pass 1: settle for 2 stages
+        for (int i = 0; i < nc; ++i) {
+          const int R = cand[i][0] * cand[i][1] * cand[i][2];
+          if (R % R0 != 0 || R > 256) continue;
+          if (cand[i][0] > st.grid_found[0] || cand[i][1] > st.grid_found[1] ||
+              cand[i][2] > st.grid_found[2])
+            continue;
+          const int capg = box_staged_rows(cand[i], st.grid_found, st.offs);
+          if (stage_ring_fit(ft, R, capg, wguess, per_cta, nsmax) >= (pass ? 2 : minns)) {
+            box[0] = cand[i][0];
+            box[1] = cand[i][1];
+            box[2] = cand[i][2];
+            break;
+          }
+        }
+    }
+    const char* es = std::getenv("BKG_STAGE_STRIP");
+    const int strip = es ? std::max(1, std::atoi(es)) : 8;
+    bool ok = false;
+    if (box[0] > 0) {
+      const int R = box[0] * box[1] * box[2];
+      ok = R % R0 == 0 && R <= 256 &&
+           stage_build(c, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, R, box, st.grid_found,
+                       strip, 32 * kStageSegLanes, st) &&
+           stage_ring_fit(ft, st.R, st.cap, st.wmax, per_cta, nsmax) >= 2;
+    }
+    if (!ok) {  // consecutive rows
+      const char* et = std::getenv("BKG_STAGE_TPW");
+      const int tpw = et ? std::max(1, std::atoi(et)) : 1;
+      const int R = std::min(256 / R0 * R0, R0 * tpw);
+      ok = stage_build(c, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, R, nullptr, nullptr, 1,
+                       32 * kStageSegLanes, st) &&
+           stage_ring_fit(ft, st.R, st.cap, st.wmax, per_cta, nsmax) >= 2;
+    }
+    if (!ok) {
+      st.R = 0;
+      st.failed_R = R0;
+      st.failed_n = n;
+      st.failed_K = K;
+      return false;
+    }
+    st.K = K;
   }
-  return false;
+  const int q = stage_ring_fit(ft, st.R, st.cap, st.wmax, per_cta, nsmax);
+  if (q < 2) return false;
+  *ns = q;
+  *smem = ft.stage_smem(st.R, st.cap, st.wmax, q);
+  return true;
 }
 
 // =========================================================== solver =====
@@ -742,7 +835,7 @@ struct bkg_solver {
     k1_run = 0;
     k1_kind = 0;
     int smem = 0;
-    if (use_stage(ctx, A, ft, &stage_ns, &smem)) {
+    if (use_stage(ctx, A, ft, k, &stage_ns, &smem)) {
       k1_kind = 2;
       ft.k1 = ft.k1_stage;
       ft.smem_k1 = smem;
@@ -797,18 +890,7 @@ struct bkg_solver {
     a.Pn = P;
     a.Pold = nullptr;
     if (fast && k1_kind == 2) {
-      const StageCsr& st = A->stage;
-      a.stg_bseg = st.bseg.ptr;
-      a.stg_bent = st.bent.ptr;
-      a.stg_segs = st.segs.ptr;
-      a.stg_vals = st.vals.ptr;
-      a.stg_lidx = st.lidx.ptr;
-      a.stg_own = st.own.ptr;
-      a.stg_nstage = stage_ns;
-      a.stg_cap = st.cap;
-      a.stg_wmax = st.wmax;
-      a.stg_first1 = 0;
-      a.stg_cnt1 = st.nblk;
+      stage_args(a, A->stage, stage_ns);
     } else if (fast && ft.sell_rows) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
       // capture: launch_chunk calls iter_args before capturing)

@@ -138,22 +138,43 @@ struct SellCsr {
 };
 
 // Staged-block copy of a CSR matrix for k1_stage (kernels_stage.cuh, built by
-// stage.cu): blocks of R consecutive rows; block b stages the row runs
-// segs[bseg[b] .. bseg[b+1]) = {first operand row, rows} into shared memory
-// (own rows start at staged index own[b]); entry (slot u, row i) of block b
-// at bent[b] + u * R + i holds the staged index (lidx, 0xFFFF = padding) and
-// the value of the row's u-th CSR entry.
+// stage.cu).  The rows are cut into blocks of R row slots: rowid[b R + i] is
+// the row in slot i of block b (-1: empty slot).  On matrices whose pattern is
+// a lexicographic grid stencil (detected from the column offsets) a block is
+// a bx x by x bz box of grid points, visited in an order that keeps the
+// neighbouring planes in L2; otherwise R consecutive rows.  Block b stages
+// the operand row runs segs[b smax .. b smax + hdr[b].nseg) = {first row,
+// rows} into shared memory; entry (slot u, row slot i) at hdr[b].ebeg + u R +
+// i holds the value (vals) of the row's u-th CSR entry and, in lidx at
+// hdr[b].ebeg + b R + u R + i, the staged index of its column (0xFFFF =
+// padding); lidx slot u = hdr[b].w holds the staged index of the row itself
+// (the Gram's P row).
+struct StageHdr {   // 32 bytes, one per block
+  int64_t ebeg;     // first entry of the block in vals (lidx: ebeg + b R)
+  int32_t nseg;     // operand row runs
+  int32_t w;        // slots = longest row of the block
+  int32_t nstaged;  // staged operand rows (sum of the run lengths)
+  int32_t pad[3];
+};
 struct StageCsr {
-  int R = 0;  // block height (0: not built)
+  int R = 0;  // row slots per block (0: not built)
   int64_t n = 0, nblk = 0;
   int cap = 0, smax = 0, wmax = 0;  // max staged rows / segments / slots per block
-  int failed_R = 0;                 // a build for (failed_R, failed_n) did not fit
+  int K = 0;                        // block-vector width the shape was chosen for
+  int box[3] = {0, 0, 0};           // grid box of a block (0: consecutive rows)
+  int64_t grid[3] = {0, 0, 0};      // grid the boxes were cut from
+  int failed_R = 0, failed_K = 0;   // a build for (R0, n, K) did not fit
   int64_t failed_n = 0;
-  DevBuf<int64_t> bseg, bent;
+  // grid_detect result for this matrix (host side, stage.cu)
+  bool grid_checked = false, has_grid = false;
+  int64_t grid_n = 0;
+  int64_t grid_found[3] = {0, 0, 0};
+  std::vector<int64_t> offs;        // sampled column offsets c - r (all signs, no 0)
+  DevBuf<StageHdr> hdr;
   DevBuf<int2> segs;
   DevBuf<uint16_t> lidx;
   DevBuf<double> vals;
-  DevBuf<int32_t> own;
+  DevBuf<int32_t> rowid;
 };
 
 }  // namespace bkg

@@ -40,10 +40,6 @@ constexpr int k1w_chunk() {
 // k1_line (line-variant sliced ELL, kernels_k1.cuh): rows per run and CSR
 // chunk (slots left after the r-1, r, r+1 entries are taken out: 4 on a
 // 7-point stencil, 2 on a 5-point one).
-// k1_stage tiles per warp per block (block height = 8 / QW x RPW x TPW rows)
-#ifndef BKG_STAGE_TPW
-#define BKG_STAGE_TPW 1
-#endif
 #ifndef BKG_K1L_RUN
 #define BKG_K1L_RUN 64
 #endif
@@ -83,11 +79,13 @@ struct FastTable {
   int rpc_k1_line = 1;  // rows per CTA pass (RPW x run per warp group)
   int line_run = 0;
   bool line_auto = false;  // the solver may pick it (measured winner for this (K, P))
-  // k1_stage alternative (TMA-staged blocks, kernels_stage.cuh): block height
-  // and its dynamic shared memory for (cap, wmax, stages)
+  // k1_stage alternative (TMA-staged blocks, kernels_stage.cuh): row slots per
+  // block are a multiple of stage_R0; its dynamic shared memory for (R, cap,
+  // wmax, stages)
   const void* k1_stage = nullptr;
-  int stage_R = 0;
-  int (*stage_smem)(int cap, int wmax, int ns) = nullptr;
+  bool stage_auto = false;  // the solver may pick it without BKG_K1_STAGE=1
+  int stage_R0 = 0;
+  int (*stage_smem)(int R, int cap, int wmax, int ns) = nullptr;
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -119,9 +117,9 @@ void fill_table(FastTable* t) {
     // B200 sweeps: k1_line wins only at K = 64, P >= 8 (C5
     // 7.42 -> 7.16 ms); at K <= 32 and K = 64, P < 8 it is 2-19% slower.
     t->line_auto = K == 64 && P >= 8;
-    t->k1_stage = (const void*)&k1_stage<K, P, W, BKG_STAGE_TPW, G>;
-    t->stage_R = StageLayout<K, P, W, BKG_STAGE_TPW>::R;
-    t->stage_smem = &k1_stage_smem<K, P, W, BKG_STAGE_TPW, G>;
+    t->k1_stage = (const void*)&k1_stage<K, P, W, G>;
+    t->stage_R0 = StageLayout<K, P, W>::R0;
+    t->stage_smem = &k1_stage_smem<K, P, W, G>;
   } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;
@@ -135,7 +133,9 @@ void fill_table(FastTable* t) {
   // DESIGN.md §5): DMMA always for P >= 8; for P < 8 the DMMA K3 wins for
   // K <= 32 (up to 1.55x) and the DMMA K2 only at P = 4; at K = 64 the scalar
   // kernels' full-line row accesses win.
-  constexpr bool MMA_OK = K % 8 == 0 && P <= 16;
+  // (a CTA's 8 warps must cover whole rows of tile groups: K / max(P, 8) <= 8;
+  // k = 128 with p <= 8 has 16 groups per row and takes the scalar kernels)
+  constexpr bool MMA_OK = K % 8 == 0 && P <= 16 && K / (P < 8 ? 8 : P) <= 8;
   constexpr bool K2_MMA = MMA_OK && (P >= 8 || (P == 4 && K <= 32));
   constexpr bool K3_MMA = MMA_OK && (P >= 8 || K <= 32);
   constexpr int RPC_MMA = 64 * (P < 8 ? 8 : P) / K;  // 8 rows x (8 warps / tile groups per row)

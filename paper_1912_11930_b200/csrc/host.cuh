@@ -16,7 +16,7 @@ void allow_smem(const void* fn, int bytes);
 int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
 // per-matrix K1 choices (api.cu): k1_stage (ring depth, smem out), k1_line
-bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int* ns, int* smem);
+bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, int* ns, int* smem);
 bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft);
 // generate.cu: device-side problem generation
 void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
@@ -24,8 +24,27 @@ void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, d
 void dev_generate_stencil_rows(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
                                uint64_t seed, double contrast, int64_t r0, int64_t r1,
                                int64_t cshift, int64_t* rowptr, int32_t* cols, double* vals);
+// stage.cu: staged-block copy for k1_stage (grid boxes or consecutive rows)
+bool grid_detect(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                 int64_t grid[3], std::vector<int64_t>* offsets = nullptr);
 bool stage_build(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
-                 const double* vals, int R, int max_segs, StageCsr& out);
+                 const double* vals, int R, const int box[3], const int64_t grid[3], int strip,
+                 int max_segs, StageCsr& out);
+// k1_stage arguments of a built StageCsr (all blocks in order; ring depth ns)
+inline void stage_args(IterArgs& a, const StageCsr& st, int ns) {
+  a.stg_hdr = st.hdr.ptr;
+  a.stg_segs = st.segs.ptr;
+  a.stg_vals = st.vals.ptr;
+  a.stg_lidx = st.lidx.ptr;
+  a.stg_rowid = st.rowid.ptr;
+  a.stg_nstage = ns;
+  a.stg_cap = st.cap;
+  a.stg_wmax = st.wmax;
+  a.stg_smax = st.smax;
+  a.stg_R = st.R;
+  a.stg_cnt = st.nblk;
+  a.stg_map = nullptr;
+}
 int64_t stencil_rows_nnz(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1);
 void dev_generate_stencil(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,
                           uint64_t seed, double contrast, bkg_matrix* m);

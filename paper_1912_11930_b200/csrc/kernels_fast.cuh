@@ -199,17 +199,16 @@ struct IterArgs {
   double* Pn;
   const double* Pold;
   // k1_stage (kernels_stage.cuh): the staged-block copy (common.cuh
-  // StageCsr), the ring depth, and the blocks of this launch --
-  // [stg_first1, +stg_cnt1) then [stg_first2, +stg_cnt2) (the partitioned
-  // solver launches interior and boundary blocks separately).
-  const int64_t* stg_bseg;
-  const int64_t* stg_bent;
+  // StageCsr), the ring depth, and the blocks of this launch -- all stg_cnt
+  // blocks in order, or stg_map[0 .. stg_cnt) (the partitioned solver
+  // launches interior and boundary blocks separately).
+  const StageHdr* stg_hdr;
   const int2* stg_segs;
   const double* stg_vals;
   const uint16_t* stg_lidx;
-  const int32_t* stg_own;
-  int stg_nstage, stg_cap, stg_wmax;
-  int64_t stg_first1, stg_cnt1, stg_first2, stg_cnt2;
+  const int32_t* stg_rowid;
+  int stg_nstage, stg_cap, stg_wmax, stg_smax, stg_R;
+  int64_t stg_cnt;
   const int64_t* stg_map;  // non-null: block j of the launch is stg_map[j]
   // dist: add this launch's alpha to red1 instead of overwriting it
   int dist_acc;

@@ -56,7 +56,7 @@ struct MmaLayout {
   static constexpr int NB = GLOBAL ? 1 : K / P;  // coefficient blocks
   static constexpr int CS = NB * P * P;
   static_assert(K % 8 == 0 && P <= 16, "DMMA path: K a multiple of 8, P <= 16");
-  static_assert(8 % Q == 0 || Q > 8, "warps per CTA must cover whole groups");
+  static_assert(8 % Q == 0, "the 8 warps of a CTA must cover whole rows of tile groups");
 };
 
 // B fragments of tile group g: frag[kc][nt] = sign * B[kc*4 + (lane&3)][nt*8 +

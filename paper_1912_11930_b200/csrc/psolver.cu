@@ -188,13 +188,15 @@ struct Part {
 };
 
 // 1 for staged blocks that read a ghost row (a segment outside [0, nloc)).
-__global__ void k_block_ghost(int64_t nblk, int64_t nloc, const int64_t* __restrict__ bseg,
-                              const int2* __restrict__ segs, unsigned char* __restrict__ flag) {
+__global__ void k_block_ghost(int64_t nblk, int64_t nloc, const StageHdr* __restrict__ hdr,
+                              int smax, const int2* __restrict__ segs,
+                              unsigned char* __restrict__ flag) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblk;
        b += (int64_t)gridDim.x * blockDim.x) {
     unsigned char f = 0;
-    for (int64_t i = bseg[b]; i < bseg[b + 1]; ++i) {
-      const int2 sg = segs[i];
+    const int ns = hdr[b].nseg;
+    for (int i = 0; i < ns; ++i) {
+      const int2 sg = segs[b * smax + i];
       if (sg.x < 0 || (int64_t)sg.x + sg.y > nloc) f = 1;
     }
     flag[b] = f;
@@ -318,16 +320,17 @@ struct bkg_psolver {
     pt.k1_kind = 0;
     pt.k1_run = 0;
     int rpc = base.rpc_k1;
-    if (use_stage(ctx, &pt.A, ft, &pt.stage_ns, &pt.smem_k1)) {
+    if (use_stage(ctx, &pt.A, ft, k, &pt.stage_ns, &pt.smem_k1)) {
       pt.k1_kind = 2;
       pt.k1 = ft.k1_stage;
       const StageCsr& st = pt.A.stage;
       DevBuf<unsigned char> flag(std::max<int64_t>(st.nblk, 1));
       int64_t nb = st.nblk, nl = pt.nloc;
-      const int64_t* bs = st.bseg.ptr;
+      const StageHdr* hd = st.hdr.ptr;
+      int sm = st.smax;
       const int2* sg = st.segs.ptr;
       unsigned char* fp = flag.ptr;
-      void* args[] = {&nb, &nl, &bs, &sg, &fp};
+      void* args[] = {&nb, &nl, &hd, &sm, &sg, &fp};
       launch(ctx, (const void*)&k_block_ghost, elem_grid(ctx, nb), 256, 0, args);
       std::vector<unsigned char> hf(st.nblk);
       d2h(ctx, hf.data(), flag.ptr, st.nblk);
@@ -491,18 +494,7 @@ struct bkg_psolver {
     a.scols = pt.A.sell.cols.ptr;
     a.svals = pt.A.sell.vals.ptr;
     a.stri = pt.k1_run ? pt.A.sell.tri.ptr : nullptr;
-    if (pt.k1_kind == 2) {
-      const StageCsr& st = pt.A.stage;
-      a.stg_bseg = st.bseg.ptr;
-      a.stg_bent = st.bent.ptr;
-      a.stg_segs = st.segs.ptr;
-      a.stg_vals = st.vals.ptr;
-      a.stg_lidx = st.lidx.ptr;
-      a.stg_own = st.own.ptr;
-      a.stg_nstage = pt.stage_ns;
-      a.stg_cap = st.cap;
-      a.stg_wmax = st.wmax;
-    }
+    if (pt.k1_kind == 2) stage_args(a, pt.A.stage, pt.stage_ns);
     return a;
   }
 
@@ -513,7 +505,7 @@ struct bkg_psolver {
     int grid = pt.g1;
     if (pt.k1_kind == 2) {
       a.stg_map = interior ? pt.map_in.ptr : pt.map_bd.ptr;
-      a.stg_cnt1 = interior ? pt.nin : pt.nbd;
+      a.stg_cnt = interior ? pt.nin : pt.nbd;
       grid = interior ? pt.g1i : pt.g1b;
     }
     void* args[] = {&a};
@@ -909,6 +901,9 @@ int bkg_psolver_part_info(const bkg_psolver* s, int part, int64_t* out) {
     out[2] = pt.k1_kind == 2 ? pt.nbd : 0;
     out[3] = pt.r0;
     out[4] = pt.r1;
+    const StageCsr& st = pt.A.stage;
+    out[5] = pt.k1_kind == 2 ? st.R : 0;
+    for (int d = 0; d < 3; ++d) out[6 + d] = pt.k1_kind == 2 ? st.box[d] : 0;
   });
 }
 

@@ -156,11 +156,12 @@ class PartitionedSolver:
     def part_info(self, part: int = 0) -> dict:
         """K1 of a part and its interior / boundary block split
         (bkg_psolver_part_info)."""
-        out = (C.c_int64 * 5)()
+        out = (C.c_int64 * 9)()
         _check(N.lib().bkg_psolver_part_info(self.handle, part, out))
         from .blockkrylov import Context
         return {"k1": Context.K1_VARIANTS[int(out[0])], "interior_blocks": int(out[1]),
-                "boundary_blocks": int(out[2]), "rows": (int(out[3]), int(out[4]))}
+                "boundary_blocks": int(out[2]), "rows": (int(out[3]), int(out[4])),
+                "block_rows": int(out[5]), "box": (int(out[6]), int(out[7]), int(out[8]))}
 
     def close(self) -> None:
         if self.handle:

@@ -158,10 +158,20 @@ def test_interior_boundary_split(ctx, monkeypatch, nparts, stage):
             assert info["k1"] == "k1_stage"
             r0, r1 = info["rows"]
             nb = info["interior_blocks"] + info["boundary_blocks"]
-            R = -(-(r1 - r0) // nb)  # block height
             nbrs = (i > 0) + (i < nparts - 1)
-            assert 0 < info["boundary_blocks"] <= nbrs * (-(-plane // R) + 1)
-            assert info["interior_blocks"] > 0
+            bx, by, bz = info["box"]
+            if bx:  # grid boxes: only the box layers next to a neighbour read ghosts
+                per_layer = -(-24 // bx) * -(-24 // by)
+                layers = -(-((r1 - r0) // plane) // bz)
+                assert nb == per_layer * layers
+                assert 0 < info["boundary_blocks"] <= min(nbrs, layers) * per_layer
+                assert info["interior_blocks"] == nb - info["boundary_blocks"]
+                if layers > nbrs:
+                    assert info["interior_blocks"] > 0
+            else:   # consecutive rows: one plane of blocks per neighbour
+                R = info["block_rows"]
+                assert 0 < info["boundary_blocks"] <= nbrs * (-(-plane // R) + 1)
+                assert info["interior_blocks"] > 0
         else:
             assert info["k1"] in ("k1_wide", "k1_line")
     s.set_rhs(b)
