@@ -105,10 +105,11 @@ void allow_smem(const void* fn, int bytes) {
     BKG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc) {
+int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc,
+                   int threads) {
   int nb = 0;
   allow_smem(fn, smem);
-  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, smem));
+  BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
   if (nb < 1) nb = 1;
   const int64_t need = std::max<int64_t>(1, (rows + rpc - 1) / rpc);
   return (int)std::min<int64_t>((int64_t)nb * c->sm_count, need);
@@ -632,7 +633,7 @@ bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K,
       const bool d3 = st.grid_found[2] > 1;
       const int(*cand)[3] = d3 ? cand3 : cand2;
       const int nc = d3 ? 8 : 7;
-      int wguess = (int)st.offs.size() + 1;
+      const int wguess = ((int)st.offs.size() + 1 + 3) / 4 * 4;
       for (int pass = 0; pass < 2 && box[0] == 0; ++pass)  // pass 1: settle for 2 stages
         for (int i = 0; i < nc; ++i) {
           const int R = cand[i][0] * cand[i][1] * cand[i][2];
@@ -799,6 +800,7 @@ struct bkg_solver {
     BKG_CUDA_CHECK(cudaHostAlloc(&h_ring, sizeof(double) * ring * k, cudaHostAllocDefault));
     if (fast) {
       choose_k1();
+      choose_resident();
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
       pcx = jac ? 1 : (precond == BKG_PRECOND_ILU0 ? 2 : 0);
@@ -821,9 +823,76 @@ struct bkg_solver {
   }
 
   int k1_kind = 0;   // 0 k1_wide, 1 k1_line, 2 k1_stage
+  int k1_threads = kThreads;  // k1_stage runs 16 warps per CTA
   int stage_ns = 0;  // k1_stage ring depth
 
-  int k1_variant() const { return !fast ? -1 : k1_kind; }
+  // Latency path (kernels_resident.cuh): small M = I systems run the whole loop
+  // in one cooperative kernel per `ring - 2` iterations.  BKG_RESIDENT=0 off.
+  bool resident = false;
+  const void* rfn = nullptr;
+  int rgrid = 0;
+  DevBuf<double> rp1, rp2;
+  DevBuf<unsigned long long> rbar;
+  DevBuf<long long> rprof;
+
+  void choose_resident() {
+    resident = false;
+    const char* env = std::getenv("BKG_RESIDENT");
+    if (!fast || precond != BKG_PRECOND_IDENTITY || (env && env[0] == '0')) return;
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    if (!coop) return;
+    for (int i = 0; i < 2 && !resident; ++i) {
+      if (!ft.resident[i]) continue;
+      const int64_t g = (n + ft.resident_rows[i] - 1) / ft.resident_rows[i];
+      int occ = 0;
+      allow_smem(ft.resident[i], ft.resident_smem);
+      BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ft.resident[i], kThreads,
+                                                                   ft.resident_smem));
+      if (occ < 1 || g > (int64_t)ctx->sm_count) continue;  // one CTA per SM
+      resident = true;
+      rfn = ft.resident[i];
+      rgrid = (int)std::max<int64_t>(g, 1);
+    }
+    if (!resident) return;
+    rp1.alloc((size_t)rgrid * ft.resident_eb1);
+    rp2.alloc((size_t)rgrid * ft.resident_eb2);
+    rbar.alloc(1);
+  }
+
+  void launch_resident(bool with_hist) {
+    ResidentArgs ra{};
+    ra.it = iter_args(with_hist);
+    ra.pbuf1 = rp1.ptr;
+    ra.pbuf2 = rp2.ptr;
+    ra.bar = rbar.ptr;
+    ra.max_steps = with_hist ? ring - 2 : (1 << 16);
+    const bool prof = std::getenv("BKG_RESIDENT_PROF") != nullptr;
+    if (prof && !rprof.ptr) {
+      rprof.alloc(12);
+      BKG_CUDA_CHECK(cudaMemsetAsync(rprof.ptr, 0, 12 * sizeof(long long), ctx->stream));
+    }
+    ra.prof = prof ? rprof.ptr : nullptr;
+    BKG_CUDA_CHECK(cudaMemsetAsync(rbar.ptr, 0, sizeof(unsigned long long), ctx->stream));
+    void* args[] = {&ra};
+    BKG_CUDA_CHECK(cudaLaunchCooperativeKernel(rfn, dim3(rgrid), dim3(kThreads), args,
+                                               (size_t)ft.resident_smem, ctx->stream));
+    ctx->launches++;
+    if (prof) {  // tuning only: CTA 0's cycles per phase, accumulated over the launches
+      long long h[12];
+      d2h(ctx, h, rprof.ptr, 12);
+      sync(ctx);
+      static const char* names[12] = {"spmm+alpha", "cta-reduce1", "barrier1", "grid-sum1",
+                                      "lambda-solve", "R-update+rho", "cta-reduce2", "barrier2",
+                                      "grid-sum2", "beta-solve", "X+stop+P", "barrier3"};
+      std::fprintf(stderr, "[resident] cycles per phase (cumulative):");
+      for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%lld", names[i], h[i]);
+      std::fprintf(stderr, "\n");
+    }
+  }
+
+  bool ran_resident = false;  // the last loop ran k_resident launches
+  int k1_variant() const { return !fast ? -1 : (ran_resident ? 3 : k1_kind); }
 
   // Per-matrix K1 choice (k1_stage, k1_line or k1_wide) and its grid.
   void choose_k1() {
@@ -834,12 +903,14 @@ struct bkg_solver {
     ft.smem_k1 = base.smem_k1;
     k1_run = 0;
     k1_kind = 0;
+    k1_threads = kThreads;
     int smem = 0;
     if (use_stage(ctx, A, ft, k, &stage_ns, &smem)) {
       k1_kind = 2;
       ft.k1 = ft.k1_stage;
       ft.smem_k1 = smem;
-      g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, A->stage.nblk, 1);
+      k1_threads = kStageThreads;
+      g1 = occupancy_grid(ctx, ft.k1, ft.smem_k1, A->stage.nblk, 1, kStageThreads);
       return;
     }
     if (use_line(ctx, A, ft)) {
@@ -936,7 +1007,7 @@ struct bkg_solver {
       const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
-      launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
+      launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, ft.k2_ilu, g2i, kThreads, ft.smem_iter, args);
       if (ev && fine) BKG_CUDA_CHECK(cudaEventRecord(ev[4], ctx->stream));
@@ -976,7 +1047,7 @@ struct bkg_solver {
       const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
-      launch(ctx, ft.k1, g1, kThreads, ft.smem_k1, args);
+      launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
@@ -1063,7 +1134,7 @@ struct bkg_solver {
   bool setup(const double* x0_host, double tol, uint64_t max_iter, bool record,
              bkg_report* rep, std::vector<double>* limits_host, bool* x0_nonzero) {
     iter_launched = 0;
-    defer = fast && BKG_DEFER_X;
+    defer = fast && BKG_DEFER_X && !resident;  // the resident loop keeps X in registers
     const size_t nk = (size_t)n * k;
     precond_ready(ctx, const_cast<bkg_matrix*>(A), precond);  // FactorizationError surfaces here
     bool x0_zero = true;
@@ -1141,9 +1212,13 @@ struct bkg_solver {
     d2h(ctx, reinterpret_cast<char*>(h_ctrl), reinterpret_cast<const char*>(dctrl()), sizeof(Ctrl));
     sync(ctx);
     uint64_t seen = 0;
+    ran_resident = false;
     while (!h_ctrl->done) {
       if (timing) {
         for (int i = 0; i < (cb ? 1 : chunk); ++i) timed_iteration(record);
+      } else if (resident && !cb) {
+        ran_resident = true;
+        launch_resident(record);
       } else if (fast && !cb) {
         launch_chunk();
       } else {
@@ -1670,7 +1745,13 @@ int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms) {
     double acc[4] = {0, 0, 0, 0};
     s->launch_iteration(false);  // warm-up
     sync(s->ctx);
+    // tuning only: BKG_STAGE_DEBUG runs K1 with parts disabled (garbage alpha ->
+    // breakdown), so the control block is reset before every profiled iteration
+    const bool dbg = std::getenv("BKG_STAGE_DEBUG") != nullptr;
     for (uint64_t i = 0; i < iterations; ++i) {
+      if (dbg)
+        h2d(s->ctx, reinterpret_cast<char*>(s->dctrl()), reinterpret_cast<const char*>(&h),
+            sizeof(Ctrl));
       s->launch_iteration(false, ev);
       BKG_CUDA_CHECK(cudaEventSynchronize(ev[3]));
       float t;
@@ -1685,7 +1766,7 @@ int bkg_solver_profile(bkg_solver* s, uint64_t iterations, double* out_ms) {
     for (int j = 0; j < 4; ++j) out_ms[j] = iterations ? acc[j] / (double)iterations : 0.0;
     d2h(s->ctx, reinterpret_cast<char*>(s->h_ctrl), reinterpret_cast<const char*>(s->dctrl()), sizeof(Ctrl));
     sync(s->ctx);
-    BKG_REQUIRE(!s->h_ctrl->done, BKG_INTERNAL, "profile pass stopped early (breakdown)");
+    BKG_REQUIRE(dbg || !s->h_ctrl->done, BKG_INTERNAL, "profile pass stopped early (breakdown)");
   });
 }
 
@@ -1703,7 +1784,7 @@ int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out) 
     if (s->fast) {
       IterArgs a = s->iter_args(false);
       void* args[] = {&a};
-      launch(s->ctx, s->ft.k1, s->g1, kThreads, s->ft.smem_k1, args);
+      launch(s->ctx, s->ft.k1, s->g1, s->k1_threads, s->ft.smem_k1, args);
     } else {
       dev_spmm(s->ctx, s->A, s->k, s->P, s->Q.ptr, nullptr, true);
     }

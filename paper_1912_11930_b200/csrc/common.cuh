@@ -146,13 +146,13 @@ struct SellCsr {
 // the operand row runs segs[b smax .. b smax + hdr[b].nseg) = {first row,
 // rows} into shared memory; entry (slot u, row slot i) at hdr[b].ebeg + u R +
 // i holds the value (vals) of the row's u-th CSR entry and, in lidx at
-// hdr[b].ebeg + b R + u R + i, the staged index of its column (0xFFFF =
-// padding); lidx slot u = hdr[b].w holds the staged index of the row itself
-// (the Gram's P row).
+// hdr[b].ebeg + b R + u R + i, the staged index of its column (padding: value
+// 0 at the row's own staged index); lidx slot u = hdr[b].w holds the staged
+// index of the row itself (the Gram's P row).
 struct StageHdr {   // 32 bytes, one per block
   int64_t ebeg;     // first entry of the block in vals (lidx: ebeg + b R)
   int32_t nseg;     // operand row runs
-  int32_t w;        // slots = longest row of the block
+  int32_t w;        // slots = longest row of the block, rounded up to 4
   int32_t nstaged;  // staged operand rows (sum of the run lengths)
   int32_t pad[3];
 };

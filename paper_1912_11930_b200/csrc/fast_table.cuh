@@ -7,6 +7,7 @@
 
 #include "kernels_fast.cuh"
 #include "kernels_k1.cuh"
+#include "kernels_resident.cuh"
 #include "kernels_stage.cuh"
 
 // K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
@@ -86,6 +87,11 @@ struct FastTable {
   bool stage_auto = false;  // the solver may pick it without BKG_K1_STAGE=1
   int stage_R0 = 0;
   int (*stage_smem)(int R, int cap, int wmax, int ns) = nullptr;
+  // latency path for small systems (kernels_resident.cuh): the whole loop as
+  // one cooperative kernel with 1 or 4 row passes per CTA
+  const void* resident[2] = {nullptr, nullptr};
+  int resident_rows[2] = {0, 0};  // rows per CTA
+  int resident_smem = 0, resident_eb1 = 0, resident_eb2 = 0;
 };
 
 // Lanes per thread: 16-byte accesses where the Gram tile stays small enough
@@ -170,6 +176,16 @@ void fill_table(FastTable* t) {
     t->k3x[2][1] = (const void*)&k3_update_xp<K, P, CPT, G, false, true, 1>;
     t->k3x[2][2] = (const void*)&k3_update_xp<K, P, CPT, G, false, true, 2>;
     t->rpc_k3 = Layout<K, P, CPT>::RPC;
+  }
+  if constexpr (K <= 16) {
+    using RS = ResidentSmem<K, P, CPT, G>;
+    t->resident[0] = (const void*)&k_resident<K, P, CPT, G, 1>;
+    t->resident[1] = (const void*)&k_resident<K, P, CPT, G, 4>;
+    t->resident_rows[0] = Layout<K, P, CPT>::RPC;
+    t->resident_rows[1] = Layout<K, P, CPT>::RPC * 4;
+    t->resident_smem = RS::bytes();
+    t->resident_eb1 = RS::EB1;
+    t->resident_eb2 = RS::EB2;
   }
   t->k2_ilu = (const void*)&k2_ilu<K, P, CPT, G>;
   t->k3 = t->k3x[0][0];

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fast_table.cuh"
 
@@ -13,7 +15,8 @@ void activate(bkg_ctx* c);
 int elem_grid(const bkg_ctx* c, int64_t total);
 void launch(bkg_ctx* c, const void* fn, int grid, int block, size_t smem, void** args);
 void allow_smem(const void* fn, int bytes);
-int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc);
+int occupancy_grid(const bkg_ctx* c, const void* fn, int smem, int64_t rows, int rpc,
+                   int threads = 256);
 bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
 // per-matrix K1 choices (api.cu): k1_stage (ring depth, smem out), k1_line
 bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, int* ns, int* smem);
@@ -44,6 +47,8 @@ inline void stage_args(IterArgs& a, const StageCsr& st, int ns) {
   a.stg_R = st.R;
   a.stg_cnt = st.nblk;
   a.stg_map = nullptr;
+  const char* dbg = std::getenv("BKG_STAGE_DEBUG");
+  a.stg_debug = dbg ? std::atoi(dbg) : 0;
 }
 int64_t stencil_rows_nnz(int kind, int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1);
 void dev_generate_stencil(bkg_ctx* c, int kind, int64_t nx, int64_t ny, int64_t nz,

@@ -73,8 +73,9 @@ __device__ __forceinline__ void st(double* p, const double (&d)[CPT]) {
 
 // Deterministic grid-wide sum of per-thread accumulators acc[NACC] over all
 // threads sharing pos = tid % TPR.  Returns true in exactly one CTA (the last
-// to arrive); there red[pos*NACC + e] holds the grid totals.
-template <int TPR, int NACC>
+// to arrive); there red[pos*NACC + e] holds the grid totals.  NTHR = threads
+// per CTA (k1_stage runs 16 warps).
+template <int TPR, int NACC, int NTHR = kThreads>
 __device__ bool grid_reduce(double (&acc)[NACC], double* red, double* partials, double* gpart,
                             uint32_t* tickets, int group) {
   constexpr int E = TPR * NACC;
@@ -87,10 +88,10 @@ __device__ bool grid_reduce(double (&acc)[NACC], double* red, double* partials, 
       for (int e = 0; e < NACC; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], off);
   }
   const bool rep = (TPR >= 32) || (lane < TPR);
-  for (int i = tid; i < E; i += kThreads) red[i] = 0.0;
+  for (int i = tid; i < E; i += NTHR) red[i] = 0.0;
   __syncthreads();
 #pragma unroll 1
-  for (int w = 0; w < kThreads / 32; ++w) {
+  for (int w = 0; w < NTHR / 32; ++w) {
     if (warp == w && rep) {
 #pragma unroll
       for (int e = 0; e < NACC; ++e) red[pos * NACC + e] += acc[e];
@@ -98,7 +99,7 @@ __device__ bool grid_reduce(double (&acc)[NACC], double* red, double* partials, 
     __syncthreads();
   }
   double* mine = partials + (size_t)blockIdx.x * E;
-  for (int i = tid; i < E; i += kThreads) mine[i] = red[i];
+  for (int i = tid; i < E; i += NTHR) mine[i] = red[i];
   __threadfence();
   __syncthreads();
   __shared__ int s_flag;
@@ -116,7 +117,7 @@ __device__ bool grid_reduce(double (&acc)[NACC], double* red, double* partials, 
   if (!s_flag) return false;
   __threadfence();
   const int c0 = g * group, c1 = min(c0 + group, nblk);
-  for (int i = tid; i < E; i += kThreads) {
+  for (int i = tid; i < E; i += NTHR) {
     double s = 0.0;
     for (int c = c0; c < c1; ++c) s += __ldcg(partials + (size_t)c * E + i);
     gpart[(size_t)g * E + i] = s;
@@ -131,7 +132,7 @@ __device__ bool grid_reduce(double (&acc)[NACC], double* red, double* partials, 
   __syncthreads();
   if (!s_flag) return false;
   __threadfence();
-  for (int i = tid; i < E; i += kThreads) {
+  for (int i = tid; i < E; i += NTHR) {
     double s = 0.0;
     for (int gg = 0; gg < ngroups; ++gg) s += __ldcg(gpart + (size_t)gg * E + i);
     red[i] = s;
@@ -208,6 +209,7 @@ struct IterArgs {
   const uint16_t* stg_lidx;
   const int32_t* stg_rowid;
   int stg_nstage, stg_cap, stg_wmax, stg_smax, stg_R;
+  int stg_debug;  // tuning only (BKG_STAGE_DEBUG): 1 skip the tile compute, 2 skip the row copies
   int64_t stg_cnt;
   const int64_t* stg_map;  // non-null: block j of the launch is stg_map[j]
   // dist: add this launch's alpha to red1 instead of overwriting it

@@ -36,6 +36,28 @@ __device__ __forceinline__ void ldg4(double (&d)[4], const double* p) {
       : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3])
       : "l"(p));
 }
+// L2 prefetch of the operand row segment a later step of this warp will
+// gather.  K1's gathers miss L2 two times out of three (ncu on C5: L2 hit rate
+// 35%) and a warp has about one step of gathers in flight, so a step costs a
+// DRAM round trip; but a warp's next step reads the same pattern shifted by a
+// constant number of rows on any shift-invariant (stencil) matrix -- the next
+// row of its run (k1_line) or the tile one grid stride ahead (k1_wide) -- so
+// each gather also prefetches "its address + that shift" into L2, and the next
+// step's gathers hit L2.  On other matrices the prefetch is a harmless guess.
+// BKG_K1_PF: 0 off; k1_line looks BKG_K1_PF rows ahead.
+#ifndef BKG_K1_PF
+#define BKG_K1_PF 0
+#endif
+#ifndef BKG_K1W_PF
+#define BKG_K1W_PF 0  // k1_wide: prefetch one grid stride ahead (costs registers: spills)
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+template <int BYTES>  // the gather's own address register + an immediate
+__device__ __forceinline__ void prefetch_l2_at(const void* p) {
+  asm volatile("prefetch.global.L2 [%0+%1];" ::"l"(p), "n"(BYTES));
+}
 __device__ __forceinline__ void stg4(double* p, const double* d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(d[0]), "d"(d[1]),
                "d"(d[2]), "d"(d[3])
@@ -92,7 +114,7 @@ template <int K, int P, int W, int CPL, bool GLOBAL>
 __device__ void gather_gram_wide(const double* red, double* blocks) {
   using L = WideLayout<K, P, W, CPL>;
   constexpr int NB = GLOBAL ? 1 : K / P;
-  for (int idx = threadIdx.x; idx < NB * P * P; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < NB * P * P; idx += blockDim.x) {
     const int blk = idx / (P * P), a = (idx / P) % P, b = idx % P;
     double s = 0.0;
     const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? K / P : blk + 1;
@@ -159,12 +181,18 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_wide(IterArgs a) {
   };
 
   // gathers + FMAs of one CSR chunk; inactive slots: v = 0, x = 0
+  // this warp's next tile is one grid stride ahead: prefetch offset in doubles,
+  // and the last column whose shifted row still exists
+  const int64_t pf_off = rstride * K;
+  const int pf_lim = (int)max((int64_t)-1, min(a.n - rstride, (int64_t)0x7fffffff));
   auto gather_fma = [&](const double (&v)[CH], const int (&c)[CH], double (&q)[CPL]) {
     double x[CH][CPL];
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       if (c[u] != kNoCol) {
-        ldg4(x[u], Pc + (int64_t)c[u] * K);
+        const double* g = Pc + (int64_t)c[u] * K;
+        ldg4(x[u], g);
+        if (BKG_K1W_PF && c[u] < pf_lim) prefetch_l2(g + pf_off);
       } else {
 #pragma unroll
         for (int t = 0; t < CPL; ++t) x[u][t] = 0.0;
@@ -345,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
       c[u] = in ? __ldg(a.scols + e) : kNoCol;
     }
   };
+  const int pf_lim = (int)max((int64_t)-1, min(a.n - BKG_K1_PF, (int64_t)0x7fffffff));
   auto load_tri = [&](int64_t s, double (&d)[4]) {
     if (s < nslice) {
       ldg4(d, a.stri + (s * RPW + rr) * 4);
@@ -358,7 +387,9 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       if (c[u] != kNoCol) {
-        ldg4(x[u], Pc + (int64_t)c[u] * K);
+        const double* g = Pc + (int64_t)c[u] * K;
+        ldg4(x[u], g);
+        if (BKG_K1_PF && c[u] < pf_lim) prefetch_l2_at<BKG_K1_PF * K * 8>(g);  // the run's row + PF
       } else {
 #pragma unroll
         for (int t = 0; t < CPL; ++t) x[u][t] = 0.0;
@@ -372,6 +403,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
   auto load_row = [&](int64_t r, double (&d)[CPL]) {
     if (r >= 0 && r < a.n) {
       ldg4(d, Pc + r * K);
+      if (BKG_K1_PF && r < pf_lim) prefetch_l2_at<BKG_K1_PF * K * 8>(Pc + r * K);
     } else {
 #pragma unroll
       for (int t = 0; t < CPL; ++t) d[t] = 0.0;

@@ -80,24 +80,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr uint16_t kNoSlot = 0xFFFF;  // padding slot of a staged block
-constexpr int kStageSegLanes = 2;     // segments per lane of the issuing warp (<= 64 / block)
+constexpr int kStageSegLanes = 2;   // segments per lane of the issuing warp (<= 64 / block)
+constexpr int kStageThreads = 512;  // 16 warps share one ring: 4 per scheduler hide the
+                                    // shared-memory latency of the slot loop (ncu at 8
+                                    // warps: 0.34 eligible warps per scheduler)
 
-// Slots per chunk and tiles interleaved per warp in the row loop (registers
-// vs shared-memory latency hiding at 8 warps per SM).
-#ifndef BKG_STAGE_U
-#define BKG_STAGE_U 4
-#endif
+// Tiles interleaved per warp in the row loop (registers: 128 at 512 threads).
 #ifndef BKG_STAGE_NT
-#define BKG_STAGE_NT 2
+#define BKG_STAGE_NT 1
 #endif
 
-// Row slots of a block are a multiple of R0: the 8 warps cover (8 / QW) row
+// Row slots of a block are a multiple of R0: the 16 warps cover (16 / QW) row
 // tiles of RPW rows x QW column slices per pass.
 template <int K, int P, int W>
 struct StageLayout {
   using L = WideLayout<K, P, W, 4>;
-  static constexpr int R0 = (kThreads / 32 / L::QW) * L::RPW;
+  static constexpr int NW = kStageThreads / 32;
+  static constexpr int R0 = (NW / L::QW) * L::RPW;
   static_assert(R0 % 8 == 0, "staged index copies need 16-byte sizes");
 };
 
@@ -122,12 +121,12 @@ __device__ __forceinline__ int2 ldg_nc_int2(const void* p) {
 }
 
 template <int K, int P, int W, bool GLOBAL>
-__global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
+__global__ void __launch_bounds__(kStageThreads, 1) k1_stage(IterArgs a) {
   using L = WideLayout<K, P, W, 4>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   constexpr int LPR = L::LPR, RPW = L::RPW, SS = L::SS, QW = L::QW;
   constexpr int R0 = StageLayout<K, P, W>::R0;
-  constexpr int NW = kThreads / 32;
+  constexpr int NW = kStageThreads / 32;
   if (stopped(a.ctrl)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rr = lane / LPR, cl = lane % LPR;
@@ -188,7 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
     }
     const int w = m_h.w;
     const int64_t ebeg = ((int64_t)m_h.y << 32) | (uint32_t)m_h.x;
-    const uint32_t bytes = (uint32_t)m_staged * K * 8 + (uint32_t)w * R * 8 +
+    const bool rows_on = !(a.stg_debug & 2);
+    const uint32_t bytes = (rows_on ? (uint32_t)m_staged * K * 8 : 0u) + (uint32_t)w * R * 8 +
                            (uint32_t)(w + 1) * R * 2 + (uint32_t)R * 4;
     uint64_t* b = bar + s;
     unsigned char* st = smraw + (size_t)s * sbytes;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < kStageSegLanes; ++t)
-      if (m_seg[t].y > 0)
+      if (m_seg[t].y > 0 && rows_on)
         bulk_g2s(st + (size_t)off[t] * K * 8, a.P + (int64_t)m_seg[t].x * K,
                  (uint32_t)m_seg[t].y * K * 8, b);
     if (lane == 0 && w > 0) bulk_g2s(st + off_vals, a.stg_vals + ebeg, (uint32_t)w * R * 8, b);
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
     // NT row tiles of this warp at a time: slot loop, Q store, Gram
     auto tiles = [&](auto ntc, int tt0) {
       constexpr int NT = decltype(ntc)::value;
-      constexpr int U = BKG_STAGE_U;
+      constexpr int U = 4;  // the builder pads every block's slots to a multiple of 4
       int rl[NT];
       double q[NT][4];
 #pragma unroll
@@ -262,22 +262,17 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
         for (int t = 0; t < NT; ++t)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const bool in = u0 + u < w;
-            li[t][u] = in ? lidx[(u0 + u) * R + rl[t]] : kNoSlot;
-            v[t][u] = in ? vals[(u0 + u) * R + rl[t]] : 0.0;
+            li[t][u] = lidx[(u0 + u) * R + rl[t]];
+            v[t][u] = vals[(u0 + u) * R + rl[t]];
           }
         double2 x[NT][U][2];
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            if (li[t][u] != kNoSlot) {
-              const double* xr = rows + li[t][u] * K;
-              x[t][u][0] = *reinterpret_cast<const double2*>(xr + c0);
-              x[t][u][1] = *reinterpret_cast<const double2*>(xr + c1);
-            } else {
-              x[t][u][0] = x[t][u][1] = make_double2(0.0, 0.0);
-            }
+            const double* xr = rows + li[t][u] * K;
+            x[t][u][0] = *reinterpret_cast<const double2*>(xr + c0);
+            x[t][u][1] = *reinterpret_cast<const double2*>(xr + c1);
           }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -314,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
           for (int pi = 0; pi < L::NPAIR; ++pi) {
             int at, bt;
             wide_pair<K, P, W, 4>(pi, at, bt);
-            const double av = oi != kNoSlot ? pr[at * 8] : 0.0;
+            const double av = pr[at * 8];  // an empty row slot has Q = 0
             const int qc = bt * 8 + (lane >> 2);  // logical column -> scratch column
             const double bv = qr[qc < W / 2 ? qc : qc + 2];
             double d[2] = {acc[2 * pi], acc[2 * pi + 1]};
@@ -326,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
         __syncwarp();
       }
     };
-    int tt = 0;
+    int tt = (a.stg_debug & 1) ? tpw : 0;
     if constexpr (BKG_STAGE_NT > 1) {
 #pragma unroll 1
       for (; tt + BKG_STAGE_NT <= tpw; tt += BKG_STAGE_NT)
@@ -348,14 +343,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_stage(IterArgs a) {
   }
   __syncthreads();  // the stages are reused as the reduction buffer
   double* red = reinterpret_cast<double*>(smraw);
-  if (!grid_reduce<L::TPR, L::NACC>(acc, red, a.partials, a.gpart, a.ctrl->tickets, a.group))
+  if (!grid_reduce<L::TPR, L::NACC, kStageThreads>(acc, red, a.partials, a.gpart,
+                                                   a.ctrl->tickets, a.group))
     return;
   double* alpha = red + L::RED;
   double* ws = alpha + 3 * S::CS;
   gather_gram_wide<K, P, W, 4, GLOBAL>(red, alpha);
   __syncthreads();
   if (a.dist) {
-    for (int i = threadIdx.x; i < S::CS; i += kThreads)
+    for (int i = threadIdx.x; i < S::CS; i += kStageThreads)
       a.red1[i] = (a.dist_acc ? a.red1[i] : 0.0) + alpha[i];
     return;
   }
@@ -368,9 +364,10 @@ template <int K, int P, int W, bool GLOBAL>
 int k1_stage_smem(int R, int cap, int wmax, int ns) {
   using L = WideLayout<K, P, W, 4>;
   using S = FastSmem<K, P, 1, GLOBAL>;
-  const int main = ns * stage_bytes(K, R, cap, wmax) + (kThreads / 32) * L::RPW * L::SS * 8 +
+  const int main = ns * stage_bytes(K, R, cap, wmax) + (kStageThreads / 32) * L::RPW * L::SS * 8 +
                    ns * 8 + ns * 8;
-  const int epi = (int)sizeof(double) * (L::RED + 3 * S::CS + bsolve_ws_doubles(P, kThreads) + K);
+  const int epi =
+      (int)sizeof(double) * (L::RED + 3 * S::CS + bsolve_ws_doubles(P, kStageThreads) + K);
   return main > epi ? main : epi;
 }
 

@@ -345,7 +345,7 @@ struct bkg_psolver {
       h2d(ctx, pt.map_bd.ptr, bd.data(), bd.size());
       int occ = 1;
       allow_smem(pt.k1, pt.smem_k1);
-      BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt.k1, kThreads,
+      BKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pt.k1, kStageThreads,
                                                                    pt.smem_k1));
       occ = std::max(occ, 1);
       const char* hs = std::getenv("BKG_HALO_SMS");
@@ -509,7 +509,7 @@ struct bkg_psolver {
       grid = interior ? pt.g1i : pt.g1b;
     }
     void* args[] = {&a};
-    launch(ctx, pt.k1, grid, kThreads, pt.smem_k1, args);
+    launch(ctx, pt.k1, grid, pt.k1_kind == 2 ? kStageThreads : kThreads, pt.smem_k1, args);
   }
 
   void iteration(bool with_hist) {

@@ -17,8 +17,9 @@
 // indices and its own rows (the Gram's P rows).  Runs of consecutive columns
 // become segments {first row, rows}; entry (slot u of row slot i, CSR order)
 // stores the index of its column inside the staged set (uint16) and its value,
-// slot-major, padded with 0xFFFF / 0.0 up to the block's longest row; one more
-// index slot holds the staged position of the row itself.
+// slot-major, padded with (the row's own staged index, 0.0) up to the block's
+// longest row rounded up to 4 slots; one more index slot holds the staged
+// position of the row itself (empty row slots: index 0, values 0).
 //
 // One warp per block merges the R sorted rows (CSR columns ascend,
 // sparse_matrix.hpp:99-105) and the own rows: each step takes the warp-wide
@@ -40,7 +41,7 @@ namespace bkg {
 
 namespace {
 
-constexpr uint16_t kNoSlotB = 0xFFFF;
+constexpr int kStageSlotPad = 4;  // slots per block padded to the kernel's chunk
 
 // rowid[b R + i]: consecutive rows (bx == 0) or grid boxes in strip order.
 __global__ void k_stage_rowid(int64_t n, int R, int64_t nblk, int64_t nx, int64_t ny, int64_t nz,
@@ -100,6 +101,10 @@ __global__ void k_stage_merge(int pass, int R, int64_t nblk, int smax,
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+    w = (w + kStageSlotPad - 1) / kStageSlotPad * kStageSlotPad;
+    int oidx[RL];  // staged index of the row itself (0 for an empty slot)
+#pragma unroll
+    for (int t = 0; t < RL; ++t) oidx[t] = 0;
     int cnt = 0, nseg = 0, last = 0, seg_first = 0, seg_len = 0;
     const int64_t ebase = pass ? hdr[b].ebeg : 0;
     const int64_t lbase = ebase + b * R;
@@ -131,7 +136,7 @@ __global__ void k_stage_merge(int pass, int R, int64_t nblk, int smax,
           head[t] = e[t] < ee[t] ? cols[e[t]] : INT_MAX;
         }
         if (ohead[t] == h) {
-          if (pass) lidx[lbase + (int64_t)w * R + lane + 32 * t] = (uint16_t)min(cnt, 0xFFFE);
+          oidx[t] = min(cnt, 0xFFFE);
           ohead[t] = INT_MAX;
         }
       }
@@ -141,16 +146,18 @@ __global__ void k_stage_merge(int pass, int R, int64_t nblk, int smax,
     if (pass) {
       if (lane == 0 && cnt > 0) sg[nseg - 1] = make_int2(seg_first, seg_len);
       for (int j = nseg + lane; j < smax; j += 32) sg[j] = make_int2(0, 0);
-      // padding slots: rows shorter than w, empty row slots
+      // the row's own staged index (slot w), and the padding slots (rows
+      // shorter than w, empty row slots): value 0 times the row's own operand
+      // row -- a valid staged row, so the kernel's slot loop has no predicates
 #pragma unroll
       for (int t = 0; t < RL; ++t) {
         const int rl = lane + 32 * t;
         if (rl >= R) continue;
+        lidx[lbase + (int64_t)w * R + rl] = (uint16_t)oidx[t];
         for (int64_t u = ee[t] - es[t]; u < w; ++u) {
-          lidx[lbase + u * R + rl] = kNoSlotB;
+          lidx[lbase + u * R + rl] = (uint16_t)oidx[t];
           svals[ebase + u * R + rl] = 0.0;
         }
-        if (rowid[b * R + rl] < 0) lidx[lbase + (int64_t)w * R + rl] = kNoSlotB;
       }
     } else if (lane == 0) {
       cnt_seg[b] = nseg;

@@ -108,7 +108,7 @@ def test_line_solve_meets_parity_bars(port, monkeypatch, k, p, glob):
 
 def test_line_and_wide_agree_on_large_system(monkeypatch):
     """At the C5 kernel table (3D 7-point 96^3, k = 64, p = 16), a
-    fixed-iteration solve with the solver's own choice (k1_stage), k1_line
+    fixed-iteration solve with the solver's own choice, k1_stage, k1_line
     and k1_wide: the K1s sum a row's products in different orders only."""
     a = bk.stencil(3, 96, 96, 96, seed=11)
     n = a.n()
@@ -130,9 +130,12 @@ def test_line_and_wide_agree_on_large_system(monkeypatch):
         out[v] = (res.x, np.array(res.report.defect_history))
         kernels[v] = ctx.last_k1()
         ctx.close()
-    assert kernels == {"auto": "k1_stage", "1": "k1_line", "0": "k1_wide", "stage": "k1_stage"}
+    auto = kernels.pop("auto")
+    assert kernels == {"1": "k1_line", "0": "k1_wide", "stage": "k1_stage"}
+    assert auto in ("k1_line", "k1_stage")  # never the row-order k1_wide at this size
     for v in ("auto", "0", "stage"):
         assert _drift(out[v][1], out["1"][1]) <= 1e-9
         xr = np.linalg.norm(out[v][0] - out["1"][0], axis=0) / np.linalg.norm(out["1"][0], axis=0)
         assert np.max(xr) <= 1e-9, xr
-    assert out["auto"][0].tobytes() == out["stage"][0].tobytes()  # auto picks k1_stage here
+    same = "stage" if auto == "k1_stage" else "1"
+    assert out["auto"][0].tobytes() == out[same][0].tobytes()  # deterministic per kernel
