@@ -54,6 +54,17 @@ __device__ __forceinline__ void ldg4(double (&d)[4], const double* p) {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+// Bulk L2 prefetch by the async copy engine (no L1 / LSU miss resources): one
+// lane asks for `bytes` starting at p.  k1_line: every BKG_K1_BPF rows of a run
+// the first lane of each lane group prefetches the next BKG_K1_BPF operand rows
+// of each of its gather streams (the run's own rows and each slot's column +
+// BKG_K1_BPF: exact on shift-invariant patterns, a harmless guess otherwise).
+#ifndef BKG_K1_BPF
+#define BKG_K1_BPF 0
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 template <int BYTES>  // the gather's own address register + an immediate
 __device__ __forceinline__ void prefetch_l2_at(const void* p) {
   asm volatile("prefetch.global.L2 [%0+%1];" ::"l"(p), "n"(BYTES));
@@ -461,6 +472,15 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
       }
       double xp[CPL];
       load_row(row + 1, xp);
+      if (BKG_K1_BPF && (t % (BKG_K1_BPF ? BKG_K1_BPF : 1)) == 0 && cl == 0 && warp % L::QW == 0) {
+        constexpr int64_t D = BKG_K1_BPF;
+        const uint32_t bytes = (uint32_t)(D * K * 8);
+        if (row + 1 + 2 * D <= a.n) bulk_prefetch_l2(a.P + (row + 1 + D) * K, bytes);
+#pragma unroll
+        for (int u = 0; u < CH; ++u)
+          if (c[u] != kNoCol && (int64_t)c[u] + 2 * D <= a.n)
+            bulk_prefetch_l2(a.P + ((int64_t)c[u] + D) * K, bytes);
+      }
       const int64_t s2 = next_of(s1);
       int64_t b2;
       int w2;
