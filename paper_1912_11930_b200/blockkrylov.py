@@ -115,7 +115,7 @@ class Context:
         _check(N.lib().bkg_ctx_launch_count(self.handle, C.byref(v)))
         return v.value
 
-    K1_VARIANTS = {-1: "exact", 0: "k1_wide", 1: "k1_line", 2: "k1_stage", 3: "resident"}
+    K1_VARIANTS = {-1: "exact", 0: "k1_wide", 1: "k1_line", 2: "k1_stage", 3: "resident", 4: "k1_grid"}
 
     def last_k1(self) -> str:
         """K1 kernel of this context's last bcg_solve (bkg_solve_k1_variant)."""

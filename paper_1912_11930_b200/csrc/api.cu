@@ -684,6 +684,36 @@ bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K,
   return true;
 }
 
+// K1 = k1_grid (kernels_grid.cuh) when the matrix is exactly a 3-D 7- or
+// 27-point constant-coefficient grid stencil (grid.cu) and the shape has the
+// kernel (K a multiple of 16, P <= 16).  BKG_K1_GRID=0/1 forces it off/on;
+// by default it is taken for systems of at least 2^16 rows (below that the
+// latency kernels win).  Out: the plan, the persistent grid, dynamic smem.
+bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g,
+                   int* ctas, int* smem) {
+  if (!ft.k1_grid[0] || A->n == 0) return false;
+  const char* env = std::getenv("BKG_K1_GRID");
+  if (env && env[0] == '0') return false;
+  if (!env && (!ft.grid_auto || A->n < (1u << 16))) return false;
+  const char* st_env = std::getenv("BKG_K1_STAGE");
+  const char* ln_env = std::getenv("BKG_K1_LINE");
+  if (!env && ((st_env && st_env[0] == '1') || (ln_env && ln_env[0] == '1')))
+    return false;  // an explicit request for another K1 wins over the default
+  const GridStencil& st = grid_stencil(c, A);
+  if (!st.ok) return false;
+  int optin = 0;
+  BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const int per_cta = std::min(optin, 227 * 1024);
+  const char* en = std::getenv("BKG_GRID_NS");
+  int ns = en ? std::max(2, std::atoi(en)) : 5;
+  while (ns > 2 && ft.grid_smem(ns) > per_cta) --ns;
+  if (ft.grid_smem(ns) > per_cta) return false;
+  grid_plan(st, K, c->sm_count, ns, g, ctas);
+  *smem = ft.grid_smem(ns);
+  allow_smem(ft.k1_grid[st.full27 ? 1 : 0], *smem);
+  return true;
+}
+
 // =========================================================== solver =====
 struct bkg_solver {
   bkg_ctx* ctx = nullptr;
@@ -822,7 +852,13 @@ struct bkg_solver {
     }
   }
 
-  int k1_kind = 0;   // 0 k1_wide, 1 k1_line, 2 k1_stage
+  int k1_kind = 0;   // 0 k1_wide, 1 k1_line, 2 k1_stage, 4 k1_grid
+  // k1_grid (kernels_grid.cuh): plan and one TMA tensor map per P buffer
+  GridArgs grid_args{};
+  struct alignas(64) TensorMap {
+    unsigned char bytes[128];
+  };
+  std::vector<std::pair<const double*, TensorMap>> grid_maps;
   int k1_threads = kThreads;  // k1_stage runs 16 warps per CTA
   int stage_ns = 0;  // k1_stage ring depth
 
@@ -905,6 +941,14 @@ struct bkg_solver {
     k1_kind = 0;
     k1_threads = kThreads;
     int smem = 0;
+    if (use_grid(ctx, A, ft, k, &grid_args, &g1, &smem)) {
+      k1_kind = 4;
+      ft.k1 = ft.k1_grid[A->gridst.full27 ? 1 : 0];
+      ft.smem_k1 = smem;
+      k1_threads = kGridThreads;
+      grid_maps.clear();
+      return;
+    }
     if (use_stage(ctx, A, ft, k, &stage_ns, &smem)) {
       k1_kind = 2;
       ft.k1 = ft.k1_stage;
@@ -936,6 +980,26 @@ struct bkg_solver {
       cudaGraphExecDestroy(graph);
       graph = nullptr;
     }
+  }
+
+  // K1 launch: k1_grid takes its plan and the tensor map of the P it reads
+  // (the deferred-X loop alternates two P buffers) as extra parameters.
+  void launch_k1(IterArgs& a) {
+    if (k1_kind == 4) {
+      TensorMap* tm = nullptr;
+      for (auto& e : grid_maps)
+        if (e.first == a.P) tm = &e.second;
+      if (!tm) {
+        grid_maps.emplace_back(a.P, TensorMap{});
+        tm = &grid_maps.back().second;
+        grid_tensor_map(a.P, k, A->gridst, tm->bytes);
+      }
+      void* args[] = {&a, &grid_args, tm->bytes};
+      launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
+      return;
+    }
+    void* args[] = {&a};
+    launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
   }
 
   IterArgs iter_args(bool with_hist) {
@@ -1007,7 +1071,7 @@ struct bkg_solver {
       const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
-      launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
+      launch_k1(a);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, ft.k2_ilu, g2i, kThreads, ft.smem_iter, args);
       if (ev && fine) BKG_CUDA_CHECK(cudaEventRecord(ev[4], ctx->stream));
@@ -1047,7 +1111,7 @@ struct bkg_solver {
       const void* k3 = k3_for(a);
       void* args[] = {&a};
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
-      launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
+      launch_k1(a);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
       launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
@@ -1783,8 +1847,7 @@ int bkg_solver_debug_first_step(bkg_solver* s, double* q_out, double* coef_out) 
     h2d(s->ctx, reinterpret_cast<char*>(s->dctrl()), reinterpret_cast<const char*>(&h), sizeof(Ctrl));
     if (s->fast) {
       IterArgs a = s->iter_args(false);
-      void* args[] = {&a};
-      launch(s->ctx, s->ft.k1, s->g1, s->k1_threads, s->ft.smem_k1, args);
+      s->launch_k1(a);
     } else {
       dev_spmm(s->ctx, s->A, s->k, s->P, s->Q.ptr, nullptr, true);
     }
@@ -1799,7 +1862,9 @@ int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
     const double nk8 = 8.0 * (double)s->n * s->k;
     const double csr = 12.0 * (double)s->A->nnz + 8.0 * (double)(s->n + 1);
     if (s->fast) {
-      out[0] = 2.0 * nk8 + csr;  // K1: read P (once, neighbours via L1/L2); write Q; CSR
+      // K1: read P (once, neighbours via L1/L2); write Q; the CSR stream --
+      // which k1_grid never reads (constant stencil): not counted for it
+      out[0] = 2.0 * nk8 + (s->k1_kind == 4 ? 0.0 : csr);
       const double jac = s->precond == BKG_PRECOND_JACOBI ? 8.0 * (double)s->n : 0.0;
       out[1] = 3.0 * nk8 + jac;  // K2: read Q, R; write R (+ D^-1 for Jacobi)
       // K3: read P, X, R; write P, X (+ D^-1); deferred X: skip launches read

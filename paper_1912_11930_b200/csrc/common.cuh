@@ -177,6 +177,18 @@ struct StageCsr {
   DevBuf<int32_t> rowid;
 };
 
+// Constant-coefficient grid stencil found in a CSR matrix (grid.cu): the
+// matrix is exactly c[dz+1][(dy+1)*3 + dx+1] on offset (dx, dy, dz) of a
+// lexicographic nx x ny x nz grid with the rows at the faces truncated.
+// k1_grid (kernels_grid.cuh) applies it from TMA-tiled operand planes.
+struct GridStencil {
+  bool checked = false, ok = false;
+  int64_t n = 0;
+  int nx = 0, ny = 0, nz = 0;
+  bool full27 = false;  // entries off the 7-point star
+  double c[3][9] = {};
+};
+
 }  // namespace bkg
 
 struct bkg_matrix;
@@ -222,6 +234,7 @@ struct bkg_matrix {
   mutable bkg::SellCsr sell;
   // staged-block copy for k1_stage (built lazily by the first fast solve)
   mutable bkg::StageCsr stage;
+  mutable bkg::GridStencil gridst;  // k1_grid: verified stencil structure (lazily)
   mutable int64_t tri_nnz = -1;  // entries in columns r - 1 .. r + 1 (counted lazily)
   // preconditioner data (built lazily on device)
   bkg::DevBuf<double> inv_diag;  // jacobi scaling or ILU 1/U(r,r)

@@ -9,6 +9,7 @@
 #include "kernels_k1.cuh"
 #include "kernels_resident.cuh"
 #include "kernels_stage.cuh"
+#include "kernels_grid.cuh"
 
 // K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
 #ifndef BKG_K1_IMPL
@@ -87,6 +88,11 @@ struct FastTable {
   bool stage_auto = false;  // the solver may pick it without BKG_K1_STAGE=1
   int stage_R0 = 0;
   int (*stage_smem)(int R, int cap, int wmax, int ns) = nullptr;
+  // k1_grid alternative (constant-coefficient grid stencils from TMA-tiled
+  // planes, kernels_grid.cuh): [0] 7-point, [1] 27-point
+  const void* k1_grid[2] = {nullptr, nullptr};
+  bool grid_auto = false;  // the solver may pick it without BKG_K1_GRID=1
+  int (*grid_smem)(int ns) = nullptr;
   // latency path for small systems (kernels_resident.cuh): the whole loop as
   // one cooperative kernel with 1 or 4 row passes per CTA
   const void* resident[2] = {nullptr, nullptr};
@@ -126,6 +132,12 @@ void fill_table(FastTable* t) {
     t->k1_stage = (const void*)&k1_stage<K, P, W, G>;
     t->stage_R0 = StageLayout<K, P, W>::R0;
     t->stage_smem = &k1_stage_smem<K, P, W, G>;
+    if constexpr (K % kGridW == 0 && K <= 64) {
+      t->k1_grid[0] = (const void*)&k1_grid<K, P, G, false>;
+      t->k1_grid[1] = (const void*)&k1_grid<K, P, G, true>;
+      t->grid_smem = &k1_grid_smem<K, P, G>;
+      if (32 * 8 * (K / kGridW) > t->e_iter) t->e_iter = 32 * 8 * (K / kGridW);
+    }
   } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram
     constexpr int W = K >= 16 ? 16 : 8;
     t->k1 = (const void*)&k1_tile<K, P, W, G>;

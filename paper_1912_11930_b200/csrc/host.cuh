@@ -21,6 +21,12 @@ bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
 // per-matrix K1 choices (api.cu): k1_stage (ring depth, smem out), k1_line
 bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, int* ns, int* smem);
 bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft);
+bool use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g, int* ctas,
+              int* smem);
+// grid.cu: constant-coefficient grid stencil detection, k1_grid plan and tensor map
+const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A);
+void grid_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, int* ctas);
+void grid_tensor_map(const double* P, int K, const GridStencil& st, void* out);
 // generate.cu: device-side problem generation
 void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
                       int64_t row0 = 0);

@@ -1,0 +1,305 @@
+// kernels_grid.cuh — K1 for constant-coefficient grid stencils, the operand
+// planes tiled through shared memory by TMA tensor copies: Q = A P
+// (kernels.hpp:129-157), alpha = <<P, Q>> (kernels.hpp:59-88), last CTA:
+// lambda = alpha^-1 rho_prev (kernels.hpp:231-240).
+//
+// When the CSR matrix is *exactly* a 7- or 27-point stencil with one value per
+// offset on a lexicographic nx x ny x nz grid, boundary rows truncated
+// (verified entry by entry on device, grid.cu: BASELINE configs C2, C4, C5),
+// row (x, y, z) of A P is sum_o c[o] P[(x, y, z) + o] with P = 0 outside the
+// grid.  P (n x K row-major) is then a 4-D tensor (column, x, y, z) and a
+// 16 x 16 tile of one z-plane plus its one-point halo, 16 columns wide, is ONE
+// cp.async.bulk.tensor.4d copy (box 16 x 18 x 18 x 1, SWIZZLE_128B; the halo
+// outside the grid is zero-filled by the TMA unit, which is exactly the
+// truncated row).  No CSR index or value is read in the loop.
+//
+// Work item = (z-chunk, tile, 16-column slice); CTA j of a persistent grid
+// takes items j, j + grid, ... (slice fastest, then x tiles: concurrently
+// running CTAs share their halos in L2).  The item's planes z0-1 .. z1 stream
+// through a ring of NS stages (one mbarrier each); the last of the 16 warps to
+// finish a stage (a shared-memory counter) issues the copy of the plane NS
+// steps ahead into it, so no warp ever waits for a free stage and there is no
+// CTA-wide barrier in the loop.  Warp w owns tile row y = w: 16 points x 16
+// columns as four "row groups" of 4 points (x = 8 (g>>1) + (g&1) + 2 r) whose
+// lane (r = lane & 3, m = lane >> 2) holds columns {2m, 2m+1} of point r --
+// one LDS.128 per operand point, conflict-free under the 128-byte swizzle
+// because the four points sit two box rows apart -- and which is at the same
+// time the FP64 DMMA m8n8k4 operand layout (A[m][r], B[r][m]) of the Gram
+// P^T Q over "even" / "odd" column blocks: no relayout, no scratch.
+//
+// March in z, scatter form: the 5 (7-point) or 9 (27-point) in-plane values
+// of plane t are read once and feed rows t-1 (their dz = +1 terms: the row is
+// complete, stored and added to the Gram), t and t+1, so an operand point is
+// read from shared memory 5 / 9 times instead of 7 / 27.  A row's products
+// are summed plane by plane (dz = -1, 0, +1), a different order from the CSR
+// kernels: fast-mode parity bars only.
+#pragma once
+
+#include <cuda.h>
+
+#include "kernels_stage.cuh"
+
+namespace bkg {
+
+constexpr int kGridBX = 16, kGridBY = 16;  // tile of grid points per plane
+constexpr int kGridWarps = kGridBY;        // compute warps: one per tile row
+constexpr int kGridThreads = kGridWarps * 32;  // 4 warps per scheduler: 128 registers
+constexpr int kGridW = 16;                 // columns per slice (128-byte box rows)
+constexpr int kGridPitch = kGridBX + 2;    // box rows per tile row
+constexpr int kGridBoxRows = kGridPitch * (kGridBY + 2);
+constexpr int kGridBoxBytes = kGridBoxRows * 128;
+constexpr int kGridStageBytes = (kGridBoxBytes + 1023) / 1024 * 1024;
+
+struct GridArgs {
+  int nx, ny, nz;
+  int tx, ty;       // tiles per axis
+  int zchunk, nzc;  // planes per item, items per (tile, slice)
+  int ns;           // ring depth
+  int64_t nitems;   // nzc * ty * tx * (K / 16)
+  // coefficient of offset (dx, dy, dz) at [dz + 1][(dy + 1) * 3 + (dx + 1)]
+  double c[3][9];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// one plane tile: box (16 columns, 18 x, 18 y, 1 z) at (c0, x, y, z) -> dst
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int x, int y,
+                                            int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Grid totals (red[lane * NACC + slice * 8 + (i * 2 + j) * 2 + e] = D_ij of the
+// slice, D layout) -> row-major p x p blocks.  Column c of a slice is element
+// c & 1 of column pair c >> 1.
+template <int K, int P, bool GLOBAL>
+__device__ void gather_gram_grid(const double* red, double* blocks) {
+  constexpr int NACC = 8 * (K / kGridW);
+  constexpr int NB = GLOBAL ? 1 : K / P;
+  for (int idx = threadIdx.x; idx < NB * P * P; idx += blockDim.x) {
+    const int blk = idx / (P * P), pa = (idx / P) % P, pb = idx % P;
+    double s = 0.0;
+    const int g0 = GLOBAL ? 0 : blk, g1 = GLOBAL ? K / P : blk + 1;
+    for (int g = g0; g < g1; ++g) {
+      const int ca = g * P + pa, cb = g * P + pb;  // same slice: P divides 16
+      const int sl = ca / kGridW, a = ca % kGridW, b = cb % kGridW;
+      const int lane = ((a >> 1) << 2) | (b >> 2), e = (b >> 1) & 1;
+      s += red[lane * NACC + sl * 8 + ((a & 1) * 2 + (b & 1)) * 2 + e];
+    }
+    blocks[idx] = s;
+  }
+}
+
+template <int K, int P, bool GLOBAL, bool FULL27>
+__global__ void __launch_bounds__(kGridThreads, 1)
+    k1_grid(IterArgs a, GridArgs g, const __grid_constant__ CUtensorMap tmP) {
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  constexpr int NSL = K / kGridW;
+  constexpr int NACC = 8 * NSL;
+  static_assert(K % kGridW == 0 && P <= kGridW && kGridW % P == 0, "16-column slices");
+  if (stopped(a.ctrl)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ unsigned char smdyn[];
+  // SWIZZLE_128B works on shared-memory address bits: 1024-byte aligned stages
+  unsigned char* smraw = smdyn + ((1024u - (smem_u32(smdyn) & 1023u)) & 1023u);
+  const int NS = g.ns;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)NS * kGridStageBytes);
+  int* fin = reinterpret_cast<int*>(full + NS);  // per stage: warps done with it
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      fin[s] = 0;
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int64_t G = gridDim.x;
+  const int64_t nmine = g.nitems > (int64_t)blockIdx.x ? (g.nitems - blockIdx.x + G - 1) / G : 0;
+  auto decode = [&](int64_t i, int& slice, int& x0, int& y0, int& z0, int& z1) {
+    int64_t r = blockIdx.x + i * G;
+    slice = (int)(r % NSL);
+    r /= NSL;
+    x0 = (int)(r % g.tx) * kGridBX;
+    r /= g.tx;
+    y0 = (int)(r % g.ty) * kGridBY;
+    z0 = (int)(r / g.ty) * g.zchunk;
+    z1 = min(z0 + g.zchunk, g.nz);
+  };
+  // the plane copies in issue order: planes z0-1 .. z1 of item 0, 1, ...
+  struct Cursor {
+    int64_t i;
+    int slice, x0, y0, z1, t;
+  };
+  auto cur_start = [&](Cursor& c, int64_t i) {
+    c.i = i;
+    if (i < nmine) {
+      int z0;
+      decode(i, c.slice, c.x0, c.y0, z0, c.z1);
+      c.t = z0 - 1;
+    }
+  };
+  auto cur_next = [&](Cursor& c) {
+    if (++c.t > c.z1) cur_start(c, c.i + 1);
+  };
+  auto issue = [&](const Cursor& c, int s) {  // one elected lane
+    mbar_expect_tx(full + s, kGridBoxBytes);
+    tma_load_4d(smraw + (size_t)s * kGridStageBytes, &tmP, c.slice * kGridW, c.x0 - 1, c.y0 - 1, c.t,
+                full + s);
+  };
+  Cursor ahead;  // the copy NS steps ahead of the plane being consumed
+  cur_start(ahead, 0);
+  for (int s = 0; s < NS; ++s) {
+    if (threadIdx.x == 0 && ahead.i < nmine) issue(ahead, s);
+    if (ahead.i < nmine) cur_next(ahead);
+  }
+
+  double gram[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) gram[e] = 0.0;
+
+  {
+    // ---- consumers ----
+    const int r = lane & 3, m = lane >> 2;
+    // box row of group gq's point: (warp + 1) * pitch + 1 + xg, xg = 8 (gq>>1) + (gq&1) + 2 r
+    const int ri0 = (warp + 1) * kGridPitch + 1 + 2 * r;
+    const double cz0 = g.c[1][4];
+    uint32_t j = 0;
+#pragma unroll 1
+    for (int64_t i = 0; i < nmine; ++i) {
+      int slice, x0, y0, z0, z1;
+      decode(i, slice, x0, y0, z0, z1);
+      const int gy = y0 + warp;
+      double acc_a[4][2], acc_b[4][2], pown[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        acc_a[q][0] = acc_a[q][1] = acc_b[q][0] = acc_b[q][1] = pown[q][0] = pown[q][1] = 0.0;
+      double* qbase = a.Q + slice * kGridW + 2 * m;
+#pragma unroll 1
+      for (int t = z0 - 1; t <= z1; ++t, ++j) {
+        const int s = (int)(j % NS);
+        mbar_wait(full + s, (j / NS) & 1);
+        const unsigned char* st = smraw + (size_t)s * kGridStageBytes;
+        const bool emit = t > z0;  // row t-1 belongs to this item
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int xg = 8 * (q >> 1) + (q & 1);
+          const int ri = ri0 + xg;
+          auto ld = [&](int d) {
+            const int row = ri + d;
+            return *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
+          };
+          double qa[2], na[2], nb[2], own[2];  // row t-1 (done), row t, row t+1 (started)
+          if constexpr (FULL27) {
+            double2 v[9];
+#pragma unroll
+            for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+              for (int dx = -1; dx <= 1; ++dx) v[(dy + 1) * 3 + dx + 1] = ld(dy * kGridPitch + dx);
+            qa[0] = acc_a[q][0];
+            qa[1] = acc_a[q][1];
+            na[0] = acc_b[q][0];
+            na[1] = acc_b[q][1];
+            nb[0] = nb[1] = 0.0;
+#pragma unroll
+            for (int o = 0; o < 9; ++o) {
+              qa[0] = fma(g.c[2][o], v[o].x, qa[0]);
+              qa[1] = fma(g.c[2][o], v[o].y, qa[1]);
+              na[0] = fma(g.c[1][o], v[o].x, na[0]);
+              na[1] = fma(g.c[1][o], v[o].y, na[1]);
+              nb[0] = fma(g.c[0][o], v[o].x, nb[0]);
+              nb[1] = fma(g.c[0][o], v[o].y, nb[1]);
+            }
+            own[0] = v[4].x;
+            own[1] = v[4].y;
+          } else {
+            const double2 vc = ld(0), vxm = ld(-1), vxp = ld(1), vym = ld(-kGridPitch),
+                          vyp = ld(kGridPitch);
+            // row t-1: + c(0,0,+1) P[t]; row t: c(0,0,-1) P[t-1] (acc_b) + plane terms
+            qa[0] = fma(g.c[2][4], vc.x, acc_a[q][0]);
+            qa[1] = fma(g.c[2][4], vc.y, acc_a[q][1]);
+            na[0] = fma(g.c[1][1], vym.x, acc_b[q][0]);
+            na[1] = fma(g.c[1][1], vym.y, acc_b[q][1]);
+            na[0] = fma(g.c[1][3], vxm.x, na[0]);
+            na[1] = fma(g.c[1][3], vxm.y, na[1]);
+            na[0] = fma(cz0, vc.x, na[0]);
+            na[1] = fma(cz0, vc.y, na[1]);
+            na[0] = fma(g.c[1][5], vxp.x, na[0]);
+            na[1] = fma(g.c[1][5], vxp.y, na[1]);
+            na[0] = fma(g.c[1][7], vyp.x, na[0]);
+            na[1] = fma(g.c[1][7], vyp.y, na[1]);
+            nb[0] = g.c[0][4] * vc.x;
+            nb[1] = g.c[0][4] * vc.y;
+            own[0] = vc.x;
+            own[1] = vc.y;
+          }
+          if (emit) {  // row t-1 is complete: store it, Gram with its own P (last step's centre)
+            const int gx = x0 + xg + 2 * r;
+            if (gx < g.nx && gy < g.ny) {
+              const int64_t row = ((int64_t)(t - 1) * g.ny + gy) * g.nx + gx;
+              *reinterpret_cast<double2*>(qbase + row * K) = make_double2(qa[0], qa[1]);
+            }
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj) {
+                double d[2] = {gram[(ii * 2 + jj) * 2], gram[(ii * 2 + jj) * 2 + 1]};
+                dmma(d, pown[q][ii], qa[jj]);
+                gram[(ii * 2 + jj) * 2] = d[0];
+                gram[(ii * 2 + jj) * 2 + 1] = d[1];
+              }
+          }
+          acc_a[q][0] = na[0];
+          acc_a[q][1] = na[1];
+          acc_b[q][0] = nb[0];
+          acc_b[q][1] = nb[1];
+          pown[q][0] = own[0];
+          pown[q][1] = own[1];
+        }
+        // the last warp done with stage s refills it with the plane NS steps ahead
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0 && atomicAdd(fin + s, 1) == kGridWarps - 1) {
+          fin[s] = 0;
+          if (ahead.i < nmine) issue(ahead, s);
+        }
+        if (ahead.i < nmine) cur_next(ahead);
+      }
+    }
+  }
+
+  // ---- deterministic grid reduction of the slice Grams, lambda solve ----
+  __syncthreads();  // the ring is reused as the reduction buffer
+  const int myslice = (int)(blockIdx.x % NSL);  // grid is a multiple of NSL: one slice per CTA
+  double acc[NACC];
+#pragma unroll
+  for (int sl = 0; sl < NSL; ++sl)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[sl * 8 + e] = sl == myslice ? gram[e] : 0.0;
+  double* red = reinterpret_cast<double*>(smraw);
+  if (!grid_reduce<32, NACC, kGridThreads>(acc, red, a.partials, a.gpart, a.ctrl->tickets,
+                                           a.group))
+    return;
+  double* alpha = red + 32 * NACC;
+  double* ws = alpha + 3 * S::CS;
+  gather_gram_grid<K, P, GLOBAL>(red, alpha);
+  __syncthreads();
+  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
+}
+
+// Dynamic shared memory of k1_grid with a ring of ns stages.
+template <int K, int P, bool GLOBAL>
+int k1_grid_smem(int ns) {
+  using S = FastSmem<K, P, 1, GLOBAL>;
+  const int main = ns * kGridStageBytes + ns * 8 + ns * 4;
+  const int epi = (int)sizeof(double) *
+                  (32 * 8 * (K / kGridW) + 3 * S::CS + bsolve_ws_doubles(P, kGridThreads) + K);
+  return (main > epi ? main : epi) + 1024;  // + alignment slack
+}
+
+}  // namespace bkg
