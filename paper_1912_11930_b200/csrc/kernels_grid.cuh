@@ -19,8 +19,11 @@
 // through a ring of NS stages (one mbarrier each); the last of the 16 warps to
 // finish a stage (a shared-memory counter) issues the copy of the plane NS
 // steps ahead into it, so no warp ever waits for a free stage and there is no
-// CTA-wide barrier in the loop.  Warp w owns tile row y = w: 16 points x 16
-// columns as four "row groups" of 4 points (x = 8 (g>>1) + (g&1) + 2 r) whose
+// CTA-wide barrier in the loop.  Warp w owns 8 x 2 points (x half w & 1, tile
+// rows 2 (w >> 1) + {0, 1}) x 16 columns as four "row groups" of 4 points
+// (x = 8 (w & 1) + (g & 1) + 2 r, y = 2 (w >> 1) + (g >> 1)) -- the groups'
+// neighbourhoods overlap in x and y, so a warp step reads 12 (7-point) or 16
+// (27-point) operand points per lane for its 4 rows, not 20 / 36 -- whose
 // lane (r = lane & 3, m = lane >> 2) holds columns {2m, 2m+1} of point r --
 // one LDS.128 per operand point, conflict-free under the 128-byte swizzle
 // because the four points sit two box rows apart -- and which is at the same
@@ -49,6 +52,19 @@ constexpr int kGridPitch = kGridBX + 2;    // box rows per tile row
 constexpr int kGridBoxRows = kGridPitch * (kGridBY + 2);
 constexpr int kGridBoxBytes = kGridBoxRows * 128;
 constexpr int kGridStageBytes = (kGridBoxBytes + 1023) / 1024 * 1024;
+
+// Row groups of a warp (tuning, B200 sweeps in DESIGN.md §5):
+//   1  8 x 2 points: x = 8 (w & 1) + (g & 1) + 2 r, y = 2 (w >> 1) + (g >> 1)
+//   0  16 x 1 points: x = 8 (g >> 1) + (g & 1) + 2 r, y = w
+#ifndef BKG_GRID_ARR
+#define BKG_GRID_ARR 1
+#endif
+__host__ __device__ constexpr int grid_gx(int q) {
+  return BKG_GRID_ARR ? (q & 1) : 8 * (q >> 1) + (q & 1);
+}
+__host__ __device__ constexpr int grid_gy(int q) { return BKG_GRID_ARR ? (q >> 1) : 0; }
+constexpr int kGridWinX = BKG_GRID_ARR ? 4 : 12;  // window of a lane's four points + halo
+constexpr int kGridWinY = BKG_GRID_ARR ? 4 : 3;
 
 struct GridArgs {
   int nx, ny, nz;
@@ -165,15 +181,14 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   {
     // ---- consumers ----
     const int r = lane & 3, m = lane >> 2;
-    // box row of group gq's point: (warp + 1) * pitch + 1 + xg, xg = 8 (gq>>1) + (gq&1) + 2 r
-    const int ri0 = (warp + 1) * kGridPitch + 1 + 2 * r;
-    const double cz0 = g.c[1][4];
+    // box row of group q's point: (yw + (q>>1) + 1) * pitch + 1 + xw + (q&1) + 2 r
+    const int xw = BKG_GRID_ARR ? 8 * (warp & 1) : 0, yw = BKG_GRID_ARR ? 2 * (warp >> 1) : warp;
+    const int ri0 = (yw + 1) * kGridPitch + 1 + xw + 2 * r;
     uint32_t j = 0;
 #pragma unroll 1
     for (int64_t i = 0; i < nmine; ++i) {
       int slice, x0, y0, z0, z1;
       decode(i, slice, x0, y0, z0, z1);
-      const int gy = y0 + warp;
       double acc_a[4][2], acc_b[4][2], pown[4][2];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -185,80 +200,81 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         mbar_wait(full + s, (j / NS) & 1);
         const unsigned char* st = smraw + (size_t)s * kGridStageBytes;
         const bool emit = t > z0;  // row t-1 belongs to this item
+        // Window of this lane's four points: box rows ri0 + (py-1) pitch + (px-1),
+        // px, py = 0..3.  Each operand point is read once and feeds every group
+        // q (point (1 + (q&1), 1 + (q>>1)) of the window) that has it as a
+        // neighbour: rows t-1 (qa, finished here), t (na) and t+1 (nb).
+        double qa[4][2], na[4][2], nb[4][2];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int xg = 8 * (q >> 1) + (q & 1);
-          const int ri = ri0 + xg;
-          auto ld = [&](int d) {
-            const int row = ri + d;
-            return *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
-          };
-          double qa[2], na[2], nb[2], own[2];  // row t-1 (done), row t, row t+1 (started)
-          if constexpr (FULL27) {
-            double2 v[9];
+          qa[q][0] = acc_a[q][0];
+          qa[q][1] = acc_a[q][1];
+          na[q][0] = acc_b[q][0];
+          na[q][1] = acc_b[q][1];
+          nb[q][0] = nb[q][1] = 0.0;
+        }
 #pragma unroll
-            for (int dy = -1; dy <= 1; ++dy)
+        for (int py = 0; py < kGridWinY; ++py)
 #pragma unroll
-              for (int dx = -1; dx <= 1; ++dx) v[(dy + 1) * 3 + dx + 1] = ld(dy * kGridPitch + dx);
-            qa[0] = acc_a[q][0];
-            qa[1] = acc_a[q][1];
-            na[0] = acc_b[q][0];
-            na[1] = acc_b[q][1];
-            nb[0] = nb[1] = 0.0;
+          for (int px = 0; px < kGridWinX; ++px) {
+            bool any = false;
 #pragma unroll
-            for (int o = 0; o < 9; ++o) {
-              qa[0] = fma(g.c[2][o], v[o].x, qa[0]);
-              qa[1] = fma(g.c[2][o], v[o].y, qa[1]);
-              na[0] = fma(g.c[1][o], v[o].x, na[0]);
-              na[1] = fma(g.c[1][o], v[o].y, na[1]);
-              nb[0] = fma(g.c[0][o], v[o].x, nb[0]);
-              nb[1] = fma(g.c[0][o], v[o].y, nb[1]);
+            for (int q = 0; q < 4; ++q) {
+              const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
+              if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && (FULL27 || dx == 0 || dy == 0))
+                any = true;
             }
-            own[0] = v[4].x;
-            own[1] = v[4].y;
-          } else {
-            const double2 vc = ld(0), vxm = ld(-1), vxp = ld(1), vym = ld(-kGridPitch),
-                          vyp = ld(kGridPitch);
-            // row t-1: + c(0,0,+1) P[t]; row t: c(0,0,-1) P[t-1] (acc_b) + plane terms
-            qa[0] = fma(g.c[2][4], vc.x, acc_a[q][0]);
-            qa[1] = fma(g.c[2][4], vc.y, acc_a[q][1]);
-            na[0] = fma(g.c[1][1], vym.x, acc_b[q][0]);
-            na[1] = fma(g.c[1][1], vym.y, acc_b[q][1]);
-            na[0] = fma(g.c[1][3], vxm.x, na[0]);
-            na[1] = fma(g.c[1][3], vxm.y, na[1]);
-            na[0] = fma(cz0, vc.x, na[0]);
-            na[1] = fma(cz0, vc.y, na[1]);
-            na[0] = fma(g.c[1][5], vxp.x, na[0]);
-            na[1] = fma(g.c[1][5], vxp.y, na[1]);
-            na[0] = fma(g.c[1][7], vyp.x, na[0]);
-            na[1] = fma(g.c[1][7], vyp.y, na[1]);
-            nb[0] = g.c[0][4] * vc.x;
-            nb[1] = g.c[0][4] * vc.y;
-            own[0] = vc.x;
-            own[1] = vc.y;
+            if (!any) continue;
+            const int row = ri0 + (py - 1) * kGridPitch + (px - 1);
+            const double2 v =
+                *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
+              if (dx < -1 || dx > 1 || dy < -1 || dy > 1) continue;
+              if (!(FULL27 || dx == 0 || dy == 0)) continue;
+              const int o = (dy + 1) * 3 + dx + 1;
+              na[q][0] = fma(g.c[1][o], v.x, na[q][0]);
+              na[q][1] = fma(g.c[1][o], v.y, na[q][1]);
+              if (FULL27 || o == 4) {
+                qa[q][0] = fma(g.c[2][o], v.x, qa[q][0]);
+                qa[q][1] = fma(g.c[2][o], v.y, qa[q][1]);
+                nb[q][0] = fma(g.c[0][o], v.x, nb[q][0]);
+                nb[q][1] = fma(g.c[0][o], v.y, nb[q][1]);
+              }
+              if (o == 4) {  // the group's own point: next step's Gram operand
+                acc_b[q][0] = v.x;  // parked in acc_b (dead: copied into na above)
+                acc_b[q][1] = v.y;
+              }
+            }
           }
-          if (emit) {  // row t-1 is complete: store it, Gram with its own P (last step's centre)
-            const int gx = x0 + xg + 2 * r;
+        if (emit) {  // rows t-1 are complete: store, Gram with their own P (last step's centre)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int gx = x0 + xw + grid_gx(q) + 2 * r, gy = y0 + yw + grid_gy(q);
             if (gx < g.nx && gy < g.ny) {
               const int64_t row = ((int64_t)(t - 1) * g.ny + gy) * g.nx + gx;
-              *reinterpret_cast<double2*>(qbase + row * K) = make_double2(qa[0], qa[1]);
+              *reinterpret_cast<double2*>(qbase + row * K) = make_double2(qa[q][0], qa[q][1]);
             }
 #pragma unroll
             for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
               for (int jj = 0; jj < 2; ++jj) {
                 double d[2] = {gram[(ii * 2 + jj) * 2], gram[(ii * 2 + jj) * 2 + 1]};
-                dmma(d, pown[q][ii], qa[jj]);
+                dmma(d, pown[q][ii], qa[q][jj]);
                 gram[(ii * 2 + jj) * 2] = d[0];
                 gram[(ii * 2 + jj) * 2 + 1] = d[1];
               }
           }
-          acc_a[q][0] = na[0];
-          acc_a[q][1] = na[1];
-          acc_b[q][0] = nb[0];
-          acc_b[q][1] = nb[1];
-          pown[q][0] = own[0];
-          pown[q][1] = own[1];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pown[q][0] = acc_b[q][0];
+          pown[q][1] = acc_b[q][1];
+          acc_a[q][0] = na[q][0];
+          acc_a[q][1] = na[q][1];
+          acc_b[q][0] = nb[q][0];
+          acc_b[q][1] = nb[q][1];
         }
         // the last warp done with stage s refills it with the plane NS steps ahead
         __threadfence_block();

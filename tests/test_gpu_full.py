@@ -82,7 +82,7 @@ def test_full_fast_parity_bars(name):
     assert int(r.converged) == m["converged"]
     assert xerr <= 1e-8, xerr
     if name.startswith("c5_full"):  # the C5 headline's K1 (the one bench.py times)
-        assert res.k1 in ("k1_line", "k1_stage"), res.k1
+        assert res.k1 == "k1_grid", res.k1
     if name.startswith("c3_full"):  # reorder-chaotic field (floor case)
         assert abs(r.iterations - m["iterations"]) <= max(1, int(0.05 * m["iterations"]))
     else:

@@ -21,6 +21,7 @@ SHAPES = [(16, 16, False), (16, 4, False), (16, 4, True), (16, 1, False), (32, 8
 @pytest.fixture
 def grid_on(monkeypatch):
     monkeypatch.setenv("BKG_K1_GRID", "1")
+    monkeypatch.setenv("BKG_RESIDENT", "0")  # small systems: not the latency kernel
     monkeypatch.delenv("BKG_K1_LINE", raising=False)
     monkeypatch.delenv("BKG_K1_STAGE", raising=False)
 

@@ -24,6 +24,7 @@ def k1_choice(request, monkeypatch):
     """Force one K1: k1_line, k1_wide, or k1_stage (TMA-staged blocks)."""
     monkeypatch.setenv("BKG_K1_LINE", "1" if request.param == "line" else "0")
     monkeypatch.setenv("BKG_K1_STAGE", "1" if request.param == "stage" else "0")
+    monkeypatch.setenv("BKG_K1_GRID", "0")
     return request.param
 
 
@@ -88,6 +89,7 @@ def test_line_solve_meets_parity_bars(port, monkeypatch, k, p, glob):
     iteration, iterations +-1, X 1e-8."""
     monkeypatch.setenv("BKG_K1_LINE", "1")
     monkeypatch.setenv("BKG_K1_STAGE", "0")
+    monkeypatch.setenv("BKG_K1_GRID", "0")
     a = bk.stencil(3, 40, 36, 29, seed=11)
     n = a.n()
     b = bk.normal_block_rhs(n, k, 7)
@@ -108,8 +110,9 @@ def test_line_solve_meets_parity_bars(port, monkeypatch, k, p, glob):
 
 def test_line_and_wide_agree_on_large_system(monkeypatch):
     """At the C5 kernel table (3D 7-point 96^3, k = 64, p = 16), a
-    fixed-iteration solve with the solver's own choice, k1_stage, k1_line
-    and k1_wide: the K1s sum a row's products in different orders only."""
+    fixed-iteration solve with the solver's own choice (k1_grid: the matrix
+    is a constant-coefficient grid stencil), k1_stage, k1_line and k1_wide:
+    the K1s sum a row's products in different orders only."""
     a = bk.stencil(3, 96, 96, 96, seed=11)
     n = a.n()
     b = bk.normal_block_rhs(n, 64, 7)
@@ -120,6 +123,9 @@ def test_line_and_wide_agree_on_large_system(monkeypatch):
     for v in ("auto", "1", "0", "stage"):
         monkeypatch.delenv("BKG_K1_LINE", raising=False)
         monkeypatch.delenv("BKG_K1_STAGE", raising=False)
+        monkeypatch.delenv("BKG_K1_GRID", raising=False)
+        if v != "auto":
+            monkeypatch.setenv("BKG_K1_GRID", "0")
         if v in ("1", "0"):
             monkeypatch.setenv("BKG_K1_LINE", v)
             monkeypatch.setenv("BKG_K1_STAGE", "0")
@@ -132,10 +138,15 @@ def test_line_and_wide_agree_on_large_system(monkeypatch):
         ctx.close()
     auto = kernels.pop("auto")
     assert kernels == {"1": "k1_line", "0": "k1_wide", "stage": "k1_stage"}
-    assert auto in ("k1_line", "k1_stage")  # never the row-order k1_wide at this size
+    assert auto == "k1_grid"
     for v in ("auto", "0", "stage"):
         assert _drift(out[v][1], out["1"][1]) <= 1e-9
         xr = np.linalg.norm(out[v][0] - out["1"][0], axis=0) / np.linalg.norm(out["1"][0], axis=0)
         assert np.max(xr) <= 1e-9, xr
-    same = "stage" if auto == "k1_stage" else "1"
-    assert out["auto"][0].tobytes() == out[same][0].tobytes()  # deterministic per kernel
+    monkeypatch.delenv("BKG_K1_LINE", raising=False)
+    monkeypatch.delenv("BKG_K1_STAGE", raising=False)
+    monkeypatch.delenv("BKG_K1_GRID", raising=False)
+    ctx = bk.Context(0, "fast")
+    again = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), cfg, opts, ctx=ctx)
+    ctx.close()
+    assert out["auto"][0].tobytes() == again.x.tobytes()  # deterministic per kernel
