@@ -689,6 +689,16 @@ bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K,
 // kernel (K a multiple of 16, P <= 16).  BKG_K1_GRID=0/1 forces it off/on;
 // by default it is taken for systems of at least 2^16 rows (below that the
 // latency kernels win).  Out: the plan, the persistent grid, dynamic smem.
+// Ring depth of k1_grid: BKG_GRID_NS, else 3 (B200 sweeps: deeper
+// rings let the CTAs drift apart and lose the halo rows in L2); 0: no fit.
+int bkg::grid_ring_depth(const FastTable& ft, int K, int per_cta) {
+  (void)K;
+  const char* en = std::getenv("BKG_GRID_NS");
+  int ns = en ? std::max(2, std::atoi(en)) : 3;
+  while (ns > 2 && ft.grid_smem(ns) > per_cta) --ns;
+  return ft.grid_smem(ns) > per_cta ? 0 : ns;
+}
+
 bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g,
                    int* ctas, int* smem) {
   if (!ft.k1_grid[0] || A->n == 0) return false;
@@ -704,11 +714,9 @@ bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, 
   int optin = 0;
   BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const int per_cta = std::min(optin, 227 * 1024);
-  const char* en = std::getenv("BKG_GRID_NS");
-  int ns = en ? std::max(2, std::atoi(en)) : 5;
-  while (ns > 2 && ft.grid_smem(ns) > per_cta) --ns;
-  if (ft.grid_smem(ns) > per_cta) return false;
-  grid_plan(st, K, c->sm_count, ns, g, ctas);
+  const int ns = grid_ring_depth(ft, K, per_cta);
+  if (ns < 2) return false;
+  grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, g, ctas);
   *smem = ft.grid_smem(ns);
   allow_smem(ft.k1_grid[st.full27 ? 1 : 0], *smem);
   return true;
@@ -992,7 +1000,7 @@ struct bkg_solver {
       if (!tm) {
         grid_maps.emplace_back(a.P, TensorMap{});
         tm = &grid_maps.back().second;
-        grid_tensor_map(a.P, k, A->gridst, tm->bytes);
+        grid_tensor_map(a.P, k, A->gridst.nx, A->gridst.ny, A->gridst.nz, tm->bytes);
       }
       void* args[] = {&a, &grid_args, tm->bytes};
       launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);

@@ -102,6 +102,9 @@ struct Ctrl {
   uint64_t breakdown_iteration;
   uint64_t breakdown_block;
   uint32_t tickets[64];  // [0..62] group tickets, [63] top ticket
+  // k1_grid: plane copies issued by all CTAs of the running launch (lockstep
+  // pacing, kernels_grid.cuh); zero between launches
+  unsigned long long grid_sync;
 };
 
 constexpr int kMaxTicketGroups = 63;
@@ -184,7 +187,8 @@ struct StageCsr {
 struct GridStencil {
   bool checked = false, ok = false;
   int64_t n = 0;
-  int nx = 0, ny = 0, nz = 0;
+  int nx = 0, ny = 0, nz = 0;  // nz: planes of these rows (a z-slab part: its own)
+  int zs = 0, nzg = 0;         // first global plane of the rows, planes of the global grid
   bool full27 = false;  // entries off the 7-point star
   double c[3][9] = {};
 };

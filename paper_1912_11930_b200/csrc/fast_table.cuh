@@ -132,7 +132,7 @@ void fill_table(FastTable* t) {
     t->k1_stage = (const void*)&k1_stage<K, P, W, G>;
     t->stage_R0 = StageLayout<K, P, W>::R0;
     t->stage_smem = &k1_stage_smem<K, P, W, G>;
-    if constexpr (K % kGridW == 0 && K <= 64) {
+    if constexpr (K % kGridW == 0 && K <= 128) {
       t->k1_grid[0] = (const void*)&k1_grid<K, P, G, false>;
       t->k1_grid[1] = (const void*)&k1_grid<K, P, G, true>;
       t->grid_smem = &k1_grid_smem<K, P, G>;

@@ -23,11 +23,16 @@ struct Coef27 {
 
 // Every row must hold exactly the in-grid offsets with a nonzero coefficient,
 // in ascending column order, each with the stencil's value bit for bit.
-__global__ void k_grid_check(int64_t n, int nx, int ny, int nz, const int64_t* __restrict__ rowptr,
+// Rows are global rows r0 .. r0 + n - 1 of an nx x ny x nz grid and the stored
+// columns are global - r0 (a z-slab part of psolver.cu; r0 = 0: a whole matrix).
+__global__ void k_grid_check(int64_t n, int64_t r0, int nx, int ny, int nz,
+                             const int64_t* __restrict__ rowptr,
                              const int32_t* __restrict__ cols, const double* __restrict__ vals,
                              Coef27 cf, int* __restrict__ bad) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t ng = (int64_t)nx * ny * nz;
+  for (int64_t rl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rl < n;
+       rl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = rl + r0;
     const int x = (int)(r % nx), y = (int)((r / nx) % ny), z = (int)(r / ((int64_t)nx * ny));
     int expect = 0;
     for (int o = 0; o < 27; ++o) {
@@ -36,12 +41,12 @@ __global__ void k_grid_check(int64_t n, int nx, int ny, int nz, const int64_t* _
           z + dz >= 0 && z + dz < nz)
         ++expect;
     }
-    const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
+    const int64_t e0 = rowptr[rl], e1 = rowptr[rl + 1];
     bool ok = e1 - e0 == expect;
     int64_t prev = -1;
     for (int64_t e = e0; ok && e < e1; ++e) {
-      const int64_t c = cols[e];
-      if (c <= prev || c < 0 || c >= n) {
+      const int64_t c = (int64_t)cols[e] + r0;
+      if (c <= prev || c < 0 || c >= ng) {
         ok = false;
         break;
       }
@@ -61,77 +66,107 @@ __global__ void k_grid_check(int64_t n, int nx, int ny, int nz, const int64_t* _
 
 }  // namespace
 
-// Fills A->gridst (cached per matrix): grid shape from the column offsets
-// (grid_detect), coefficients from one interior row, then the exact check.
-const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A) {
-  GridStencil& st = A->gridst;
-  const int64_t n = (int64_t)A->n;
-  if (st.checked && st.n == n) return st;
+// Rows [r0, r0 + n) of a global matrix of `nglobal` rows, stored with columns
+// global - r0: grid shape from the column offsets (grid_detect), coefficients
+// from one interior row, then the exact check of every row.  st.nz / st.zs are
+// the part's planes and its first global plane (whole matrix: r0 = 0).
+void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                       const double* vals, int64_t r0, int64_t nglobal, GridStencil& st) {
   st = GridStencil{};
   st.checked = true;
   st.n = n;
   int64_t grid[3];
-  if (n >= (int64_t)1 << 31 || !grid_detect(c, n, A->rowptr.ptr, A->cols.ptr, grid)) return st;
-  if (grid[0] < 3 || grid[1] < 3 || grid[2] < 3) return st;  // 3-D only
-  if (grid[0] > (1 << 20) || grid[1] > (1 << 20) || grid[2] > (1 << 20)) return st;
-  const int nx = (int)grid[0], ny = (int)grid[1], nz = (int)grid[2];
-  const int64_t mid = ((int64_t)(nz / 2) * ny + ny / 2) * nx + nx / 2;
+  if (nglobal >= (int64_t)1 << 31 || !grid_detect(c, n, rowptr, cols, grid)) return;
+  if (grid[0] < 3 || grid[1] < 3 || grid[2] < 1) return;
+  if (grid[0] > (1 << 20) || grid[1] > (1 << 20)) return;
+  const int nx = (int)grid[0], ny = (int)grid[1];
+  const int64_t plane = (int64_t)nx * ny;
+  if (r0 % plane != 0 || nglobal % plane != 0 || n % plane != 0) return;  // whole planes only
+  if (nglobal / plane > (1 << 20) || nglobal / plane < 3) return;  // 3-D only
+  const int nz = (int)(n / plane), nzg = (int)(nglobal / plane), zs = (int)(r0 / plane);
+  // a row away from every face of the global grid
+  int zm = nz / 2;
+  if (zs + zm < 1) zm = 1 - zs;
+  if (zs + zm > nzg - 2) zm = nzg - 2 - zs;
+  if (zm < 0 || zm >= nz) return;
+  const int64_t mid = ((int64_t)zm * ny + ny / 2) * nx + nx / 2;
   int64_t rp[2];
-  d2h(c, rp, A->rowptr.ptr + mid, 2);
+  d2h(c, rp, rowptr + mid, 2);
   sync(c);
   const int64_t cnt = rp[1] - rp[0];
-  if (cnt <= 0 || cnt > 27) return st;
+  if (cnt <= 0 || cnt > 27) return;
   std::vector<int32_t> cl(cnt);
   std::vector<double> vl(cnt);
-  d2h(c, cl.data(), A->cols.ptr + rp[0], cnt);
-  d2h(c, vl.data(), A->vals.ptr + rp[0], cnt);
+  d2h(c, cl.data(), cols + rp[0], cnt);
+  d2h(c, vl.data(), vals + rp[0], cnt);
   sync(c);
   Coef27 cf{};
   for (int64_t e = 0; e < cnt; ++e) {
-    const int64_t col = cl[e];
-    const int dx = (int)(col % nx) - nx / 2, dy = (int)((col / nx) % ny) - ny / 2,
-              dz = (int)(col / ((int64_t)nx * ny)) - nz / 2;
-    if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) return st;
-    if (vl[e] == 0.0) return st;
-    cf.c[(dz + 1) * 9 + (dy + 1) * 3 + dx + 1] = vl[e];
+    const int64_t d = (int64_t)cl[e] - mid;  // column offset of an interior row
+    // d = dz plane + dy nx + dx with |dx|, |dy|, |dz| <= 1
+    int dz = 0, dy = 0;
+    int64_t rem = d;
+    if (rem > plane / 2) dz = 1;
+    if (rem < -(plane / 2)) dz = -1;
+    rem -= dz * plane;
+    if (rem > nx / 2) dy = 1;
+    if (rem < -(nx / 2)) dy = -1;
+    rem -= (int64_t)dy * nx;
+    if (rem < -1 || rem > 1) return;
+    if (vl[e] == 0.0) return;
+    cf.c[(dz + 1) * 9 + (dy + 1) * 3 + (int)rem + 1] = vl[e];
   }
   DevBuf<int> bad(1);
   BKG_CUDA_CHECK(cudaMemsetAsync(bad.ptr, 0, sizeof(int), c->stream));
   {
-    int64_t nn = n;
-    int ax = nx, ay = ny, az = nz;
-    const int64_t* rpp = A->rowptr.ptr;
-    const int32_t* cp = A->cols.ptr;
-    const double* vp = A->vals.ptr;
+    int64_t nn = n, rr = r0;
+    int ax = nx, ay = ny, az = nzg;
     int* bp = bad.ptr;
-    void* args[] = {&nn, &ax, &ay, &az, &rpp, &cp, &vp, &cf, &bp};
+    void* args[] = {&nn, &rr, &ax, &ay, &az, &rowptr, &cols, &vals, &cf, &bp};
     launch(c, (const void*)&k_grid_check, elem_grid(c, n), 256, 0, args);
   }
   int hbad = 1;
   d2h(c, &hbad, bad.ptr, 1);
   sync(c);
-  if (hbad) return st;
+  if (hbad) return;
   st.ok = true;
   st.nx = nx;
   st.ny = ny;
   st.nz = nz;
+  st.zs = zs;
+  st.nzg = nzg;
   for (int o = 0; o < 27; ++o) {
     st.c[o / 9][o % 9] = cf.c[o];
     const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
     if (cf.c[o] != 0.0 && (dx != 0) + (dy != 0) + (dz != 0) > 1) st.full27 = true;
   }
+}
+
+// A->gridst, cached per matrix.
+const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A) {
+  GridStencil& st = A->gridst;
+  const int64_t n = (int64_t)A->n;
+  if (st.checked && st.n == n) return st;
+  grid_stencil_rows(c, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, 0, n, st);
   return st;
 }
 
 // Work plan: z-chunk length that maximises (CTA utilisation) / (1 + 2 / chunk)
 // -- each item reads two extra planes -- for a persistent grid of `ctas` CTAs
 // (a multiple of the K / 16 slices, so a CTA keeps one slice).
-void grid_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, int* ctas) {
+// Rows produced: planes [zbeg, zend) of the part; zoff = the part's plane 0 in
+// the operand tensor.
+void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int zend, int zoff,
+               GridArgs* g, int* ctas) {
   const int nsl = K / kGridW;
+  const int nzr = zend - zbeg;
   std::memset(g, 0, sizeof(*g));
   g->nx = st.nx;
   g->ny = st.ny;
   g->nz = st.nz;
+  g->zbeg = zbeg;
+  g->zend = zend;
+  g->zoff = zoff;
   g->tx = (st.nx + kGridBX - 1) / kGridBX;
   g->ty = (st.ny + kGridBY - 1) / kGridBY;
   g->ns = ns;
@@ -139,10 +174,10 @@ void grid_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, 
   const int64_t T = (int64_t)g->tx * g->ty * nsl;
   const int64_t G = std::max<int64_t>(nsl, (int64_t)(sm_count / nsl) * nsl);
   double best = -1.0;
-  int best_chunk = st.nz;
-  for (int nzc = 1; nzc <= std::max(1, st.nz / 4); ++nzc) {
-    const int chunk = (st.nz + nzc - 1) / nzc;
-    const int real = (st.nz + chunk - 1) / chunk;
+  int best_chunk = nzr;
+  for (int nzc = 1; nzc <= std::max(1, nzr / 4); ++nzc) {
+    const int chunk = (nzr + nzc - 1) / nzc;
+    const int real = (nzr + chunk - 1) / chunk;
     const int64_t items = T * real;
     const int64_t grid = std::min(G, items);
     const int64_t rounds = (items + grid - 1) / grid;
@@ -154,16 +189,43 @@ void grid_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, 
     }
   }
   const char* ez = std::getenv("BKG_GRID_ZCHUNK");
-  if (ez && std::atoi(ez) > 0) best_chunk = std::min(st.nz, std::atoi(ez));
+  if (ez && std::atoi(ez) > 0) best_chunk = std::min(nzr, std::atoi(ez));
   g->zchunk = best_chunk;
-  g->nzc = (st.nz + best_chunk - 1) / best_chunk;
+  g->zstride = best_chunk;
+  g->nzc = (nzr + best_chunk - 1) / best_chunk;
   g->nitems = T * g->nzc;
   *ctas = (int)std::min(G, g->nitems);
+  // Lockstep pacing pays over long launches only (B200 sweeps, DESIGN.md §5:
+  // C5, 28 rounds of 66 planes per CTA, 3.23 -> 3.05 ms with loose pacing; C2,
+  // 7 rounds of 18, loses 3%; one round starts in step by itself)
+  const char* es = std::getenv("BKG_GRID_SYNC");
+  const char* el = std::getenv("BKG_GRID_LEAD");
+  const int64_t rounds = (g->nitems + *ctas - 1) / *ctas;
+  g->sync_every = es ? std::atoi(es) : (rounds * (g->zchunk + 2) >= 512 ? 16 : 0);
+  g->sync_lead = el ? std::max(0, std::atoi(el)) : 1;
+}
+
+// The two single-plane items per (tile, slice) at the ends of a z-slab part:
+// planes 0 and nz - 1 (the rows that read the neighbours' ghost planes).
+void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool lower, bool upper,
+                    int zoff, GridArgs* g, int* ctas) {
+  const int first = lower ? 0 : st.nz - 1;
+  grid_plan(st, K, sm_count, ns, first, first + 1, zoff, g, ctas);
+  if (lower && upper && st.nz > 1) {
+    g->zend = st.nz;
+    g->zstride = st.nz - 1;
+    g->nzc = 2;
+    g->nitems *= 2;
+    const int nsl = K / kGridW;
+    *ctas = (int)std::min<int64_t>(std::max<int64_t>(nsl, (int64_t)(sm_count / nsl) * nsl),
+                                   g->nitems);
+  }
+  g->sync_every = 0;
 }
 
 // TMA tensor map of a row-major n x K block vector seen as (column, x, y, z),
 // box = one 16-column plane tile with its halo, 128-byte swizzle, zero fill.
-void grid_tensor_map(const double* P, int K, const GridStencil& st, void* out) {
+void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) {
   typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -177,10 +239,9 @@ void grid_tensor_map(const double* P, int K, const GridStencil& st, void* out) {
                 "cuTensorMapEncodeTiled is not available from the driver");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  const cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)st.nx, (cuuint64_t)st.ny,
-                              (cuuint64_t)st.nz};
-  const cuuint64_t strides[3] = {(cuuint64_t)K * 8, (cuuint64_t)K * 8 * st.nx,
-                                 (cuuint64_t)K * 8 * st.nx * st.ny};
+  const cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+  const cuuint64_t strides[3] = {(cuuint64_t)K * 8, (cuuint64_t)K * 8 * nx,
+                                 (cuuint64_t)K * 8 * nx * ny};
   const cuuint32_t box[4] = {kGridW, kGridBX + 2, kGridBY + 2, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult rc = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,

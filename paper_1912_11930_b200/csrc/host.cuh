@@ -25,8 +25,14 @@ bool use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridA
               int* smem);
 // grid.cu: constant-coefficient grid stencil detection, k1_grid plan and tensor map
 const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A);
-void grid_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, int* ctas);
-void grid_tensor_map(const double* P, int K, const GridStencil& st, void* out);
+void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                       const double* vals, int64_t r0, int64_t nglobal, GridStencil& st);
+void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int zend, int zoff,
+               GridArgs* g, int* ctas);
+void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool lower, bool upper,
+                    int zoff, GridArgs* g, int* ctas);
+void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out);
+int grid_ring_depth(const FastTable& ft, int K, int per_cta);
 // generate.cu: device-side problem generation
 void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
                       int64_t row0 = 0);

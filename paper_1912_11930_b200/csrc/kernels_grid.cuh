@@ -66,11 +66,28 @@ __host__ __device__ constexpr int grid_gy(int q) { return BKG_GRID_ARR ? (q >> 1
 constexpr int kGridWinX = BKG_GRID_ARR ? 4 : 12;  // window of a lane's four points + halo
 constexpr int kGridWinY = BKG_GRID_ARR ? 4 : 3;
 
+#ifndef BKG_GRID_PACE
+#define BKG_GRID_PACE 1  // 0: compile the lockstep pacing out (tuning)
+#endif
+
 struct GridArgs {
   int nx, ny, nz;
   int tx, ty;       // tiles per axis
   int zchunk, nzc;  // planes per item, items per (tile, slice)
+  // Rows produced: planes [z0, min(z0 + zchunk, zend)) for z0 = zbeg + c zstride,
+  // c < nzc (one solver: zbeg 0, zstride = zchunk, zend = nz).  The operand
+  // tensor may start zoff planes below plane 0 (a z-slab part with its ghost
+  // plane, psolver.cu): plane t is tensor plane t + zoff, and planes outside
+  // the tensor read as zero.
+  int zbeg, zend, zstride, zoff;
   int ns;           // ring depth
+  // Lockstep pacing (0: off): before issuing the copy of its step j, j a
+  // multiple of sync_every, a CTA waits until the grid as a whole has issued
+  // (j / sync_every - sync_lead) segments per CTA, so neighbouring tiles stay
+  // within a few planes of each other and read their shared halo rows from L2
+  // (without it CTAs drift apart over a launch's rounds: ncu, C5, 1.31x the
+  // operand bytes from DRAM).  Performance only: the wait times out.
+  int sync_every, sync_lead;
   int64_t nitems;   // nzc * ty * tx * (K / 16)
   // coefficient of offset (dx, dy, dz) at [dz + 1][(dy + 1) * 3 + (dx + 1)]
   double c[3][9];
@@ -143,8 +160,8 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     x0 = (int)(r % g.tx) * kGridBX;
     r /= g.tx;
     y0 = (int)(r % g.ty) * kGridBY;
-    z0 = (int)(r / g.ty) * g.zchunk;
-    z1 = min(z0 + g.zchunk, g.nz);
+    z0 = g.zbeg + (int)(r / g.ty) * g.zstride;
+    z1 = min(z0 + g.zchunk, g.zend);
   };
   // the plane copies in issue order: planes z0-1 .. z1 of item 0, 1, ...
   struct Cursor {
@@ -164,13 +181,37 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   };
   auto issue = [&](const Cursor& c, int s) {  // one elected lane
     mbar_expect_tx(full + s, kGridBoxBytes);
-    tma_load_4d(smraw + (size_t)s * kGridStageBytes, &tmP, c.slice * kGridW, c.x0 - 1, c.y0 - 1, c.t,
-                full + s);
+    tma_load_4d(smraw + (size_t)s * kGridStageBytes, &tmP, c.slice * kGridW, c.x0 - 1, c.y0 - 1,
+                c.t + g.zoff, full + s);
+  };
+  // lockstep pacing (GridArgs::sync_every): called by the issuing lane before
+  // the copy of step jn; counts this CTA into segment jn / sync_every and waits
+  // for the grid.  A CTA that has issued its last copy adds a large constant so
+  // nobody waits for it again.
+  unsigned long long* gsync = &a.ctrl->grid_sync;
+  auto pace = [&](uint32_t jn) {
+    if (!BKG_GRID_PACE) return;
+    if (g.sync_every <= 0 || jn % (uint32_t)g.sync_every != 0) return;
+    const long long seg = jn / (uint32_t)g.sync_every;
+    atomicAdd(gsync, 1ull);
+    // the ring's first NS copies are issued unpaced: segments 0 .. seg0 - 1
+    const long long seg0 = (NS - 1) / g.sync_every + 1;
+    const long long want = (seg - g.sync_lead - seg0 + 1) * (long long)G;
+    if (want <= 0) return;
+    const long long t0 = clock64();
+    while ((long long)*reinterpret_cast<volatile unsigned long long*>(gsync) < want)
+      if (clock64() - t0 > (1ll << 21)) break;  // ~1 ms: never a correctness dependency
+  };
+  auto issued_last = [&](const Cursor& c) {  // c was this CTA's final copy
+    if (BKG_GRID_PACE && g.sync_every > 0 && c.i + 1 >= nmine && c.t >= c.z1) atomicAdd(gsync, 1ull << 40);
   };
   Cursor ahead;  // the copy NS steps ahead of the plane being consumed
   cur_start(ahead, 0);
   for (int s = 0; s < NS; ++s) {
-    if (threadIdx.x == 0 && ahead.i < nmine) issue(ahead, s);
+    if (threadIdx.x == 0 && ahead.i < nmine) {
+      issue(ahead, s);
+      issued_last(ahead);
+    }
     if (ahead.i < nmine) cur_next(ahead);
   }
 
@@ -281,7 +322,11 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         __syncwarp();
         if (lane == 0 && atomicAdd(fin + s, 1) == kGridWarps - 1) {
           fin[s] = 0;
-          if (ahead.i < nmine) issue(ahead, s);
+          if (ahead.i < nmine) {
+            pace(j + NS);
+            issue(ahead, s);
+            issued_last(ahead);
+          }
         }
         if (ahead.i < nmine) cur_next(ahead);
       }
@@ -304,6 +349,12 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   double* ws = alpha + 3 * S::CS;
   gather_gram_grid<K, P, GLOBAL>(red, alpha);
   __syncthreads();
+  if (threadIdx.x == 0) *gsync = 0;  // every CTA is past its loop: ready for the next launch
+  if (a.dist) {  // row-partitioned solver: publish this part's alpha (psolver.cu)
+    for (int i = threadIdx.x; i < S::CS; i += kGridThreads)
+      a.red1[i] = (a.dist_acc ? a.red1[i] : 0.0) + alpha[i];
+    return;
+  }
   const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }

@@ -184,6 +184,14 @@ struct Part {
   DevBuf<int64_t> map_in, map_bd;  // k1_stage blocks without / with ghost rows
   int64_t nin = 0, nbd = 0;
   int g1 = 1, g1i = 1, g1b = 1, g2 = 1, g3 = 1;
+  // k1_grid (k1_kind 4, kernels_grid.cuh): the part is a z-slab of a constant
+  // grid stencil; interior planes (no ghost plane read) and the end planes
+  // are separate launches over the ghost-extended P seen as a tensor
+  GridStencil gst;
+  GridArgs ga_in{}, ga_bd{};
+  struct alignas(64) TensorMap {
+    unsigned char bytes[128];
+  } tmap[2];
   Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_buf.ptr); }
 };
 
@@ -307,6 +315,59 @@ struct bkg_psolver {
     parts.push_back(std::move(pt));
   }
 
+  // k1_grid for a part that is whole z-planes of a constant-coefficient grid
+  // stencil (grid.cu checks every row): the ghost-extended P buffers are
+  // tensors (column, x, y, plane) whose first plane is the lower ghost plane
+  // when there is one; planes that read no ghost plane run while the halo is
+  // in flight, the one or two end planes after it.  BKG_K1_GRID=0/1 forces it
+  // off/on (default: parts of >= 2^16 rows).
+  bool use_grid_part(Part& pt) {
+    if (!ft.k1_grid[0] || pt.nloc == 0) return false;
+    const char* env = std::getenv("BKG_K1_GRID");
+    if (env && env[0] == '0') return false;
+    if (!env && (!ft.grid_auto || pt.nloc < (1 << 16))) return false;
+    const char* st_env = std::getenv("BKG_K1_STAGE");
+    const char* ln_env = std::getenv("BKG_K1_LINE");
+    if (!env && ((st_env && st_env[0] == '1') || (ln_env && ln_env[0] == '1'))) return false;
+    grid_stencil_rows(ctx, pt.nloc, pt.A.rowptr.ptr, pt.A.cols.ptr, pt.A.vals.ptr, pt.r0, n,
+                      pt.gst);
+    const GridStencil& st = pt.gst;
+    if (!st.ok) return false;
+    const int64_t plane = (int64_t)st.nx * st.ny;
+    const bool lower = st.zs > 0, upper = st.zs + st.nz < st.nzg;
+    if (pt.lo != pt.r0 - (lower ? plane : 0) || pt.hi != pt.r1 + (upper ? plane : 0)) return false;
+    int optin = 0;
+    BKG_CUDA_CHECK(
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    const int ns = grid_ring_depth(ft, k, std::min(optin, 227 * 1024));
+    if (ns < 2) return false;
+    pt.k1_kind = 4;
+    pt.k1 = ft.k1_grid[st.full27 ? 1 : 0];
+    pt.smem_k1 = ft.grid_smem(ns);
+    allow_smem(pt.k1, pt.smem_k1);
+    const int zoff = lower ? 1 : 0;
+    const int zb = lower ? 1 : 0, ze = upper ? st.nz - 1 : st.nz;
+    const char* hs = std::getenv("BKG_HALO_SMS");
+    const int reserve = use_nccl && nranks > 1 ? (hs ? std::atoi(hs) : 4) : 0;
+    pt.nin = pt.nbd = 0;
+    pt.g1i = pt.g1b = 1;
+    if (ze > zb) {
+      grid_plan(st, k, std::max(1, ctx->sm_count - reserve), ns, zb, ze, zoff, &pt.ga_in,
+                &pt.g1i);
+      pt.nin = pt.ga_in.nitems;
+    }
+    if (lower || upper) {
+      const bool lo_end = lower, up_end = upper && !(lower && st.nz == 1);
+      grid_plan_ends(st, k, ctx->sm_count, ns, lo_end, up_end, zoff, &pt.ga_bd, &pt.g1b);
+      pt.nbd = pt.ga_bd.nitems;
+    }
+    pt.g1 = std::max(pt.g1i, pt.g1b);
+    const int nzt = (int)((pt.hi - pt.lo) / plane);
+    for (int i = 0; i < (defer ? 2 : 1); ++i)
+      grid_tensor_map(pt.Pext[i].ptr, k, st.nx, st.ny, nzt, pt.tmap[i].bytes);
+    return true;
+  }
+
   // K1 of a part: k1_stage with its blocks split into those that read ghost
   // rows (boundary: launched after the halo) and the rest (interior:
   // launched while the halo is in flight); else k1_line / k1_wide after the
@@ -320,6 +381,7 @@ struct bkg_psolver {
     pt.k1_kind = 0;
     pt.k1_run = 0;
     int rpc = base.rpc_k1;
+    if (use_grid_part(pt)) return;
     if (use_stage(ctx, &pt.A, ft, k, &pt.stage_ns, &pt.smem_k1)) {
       pt.k1_kind = 2;
       pt.k1 = ft.k1_stage;
@@ -508,6 +570,13 @@ struct bkg_psolver {
       a.stg_cnt = interior ? pt.nin : pt.nbd;
       grid = interior ? pt.g1i : pt.g1b;
     }
+    if (pt.k1_kind == 4) {
+      GridArgs ga = interior ? pt.ga_in : pt.ga_bd;
+      const int cur = a.P == pt.P[1] ? 1 : 0;
+      void* gargs[] = {&a, &ga, pt.tmap[cur].bytes};
+      launch(ctx, pt.k1, interior ? pt.g1i : pt.g1b, kGridThreads, pt.smem_k1, gargs);
+      return;
+    }
     void* args[] = {&a};
     launch(ctx, pt.k1, grid, pt.k1_kind == 2 ? kStageThreads : kThreads, pt.smem_k1, args);
   }
@@ -522,11 +591,12 @@ struct bkg_psolver {
     BKG_CUDA_CHECK(cudaEventRecord(ev_h, hstream));
     // K1 interior blocks overlap the halo; boundary blocks (and the other
     // K1 kernels) after it
+    auto split = [](const Part& pt) { return pt.k1_kind == 2 || pt.k1_kind == 4; };
     for (Part& pt : parts)
-      if (pt.k1_kind == 2 && pt.nin > 0) launch_k1(pt, args_of(pt, with_hist, cur), true, false);
+      if (split(pt) && pt.nin > 0) launch_k1(pt, args_of(pt, with_hist, cur), true, false);
     BKG_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ev_h, 0));
     for (Part& pt : parts) {
-      if (pt.k1_kind != 2)
+      if (!split(pt))
         launch_k1(pt, args_of(pt, with_hist, cur), false, false);
       else if (pt.nbd > 0)
         launch_k1(pt, args_of(pt, with_hist, cur), false, pt.nin > 0);
@@ -897,8 +967,8 @@ int bkg_psolver_part_info(const bkg_psolver* s, int part, int64_t* out) {
     BKG_REQUIRE(part >= 0 && part < (int)s->parts.size(), BKG_CONFIG, "psolver: no such part");
     const Part& pt = s->parts[part];
     out[0] = pt.k1_kind;
-    out[1] = pt.k1_kind == 2 ? pt.nin : 0;
-    out[2] = pt.k1_kind == 2 ? pt.nbd : 0;
+    out[1] = pt.k1_kind == 2 || pt.k1_kind == 4 ? pt.nin : 0;
+    out[2] = pt.k1_kind == 2 || pt.k1_kind == 4 ? pt.nbd : 0;
     out[3] = pt.r0;
     out[4] = pt.r1;
     const StageCsr& st = pt.A.stage;

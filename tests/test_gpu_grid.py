@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 SHAPES = [(16, 16, False), (16, 4, False), (16, 4, True), (16, 1, False), (32, 8, False),
           (32, 16, False), (32, 2, True), (64, 16, False), (64, 4, True), (64, 1, False),
-          (64, 8, False)]
+          (64, 8, False), (128, 16, False), (128, 4, True)]
 
 
 @pytest.fixture

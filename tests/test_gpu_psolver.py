@@ -148,6 +148,7 @@ def test_interior_boundary_split(ctx, monkeypatch, nparts, stage):
     the split itself: a z-slab part of a 7-point stencil has boundary blocks
     only next to its neighbours (one plane each) and no ghost reads inside."""
     monkeypatch.setenv("BKG_K1_STAGE", stage)
+    monkeypatch.setenv("BKG_K1_GRID", "0")
     case, a, b = inputs("c2_24")
     cfg = bk.SubalgebraConfig(case.k, case.p, case.mode)
     s = PartitionedSolver.virtual(a, cfg, nparts, ctx)
@@ -182,6 +183,53 @@ def test_interior_boundary_split(ctx, monkeypatch, nparts, stage):
                        bk.SolveOptions(tol=1e-300, max_iter=40, record_history=True), ctx=ctx)
     h1 = np.array(ref.report.defect_history)
     assert rep.iterations == ref.report.iterations == 40
+    assert np.max(np.abs(hist - h1) / h1) <= 1e-9
+    xr = np.linalg.norm(x - ref.x, axis=0) / np.linalg.norm(ref.x, axis=0)
+    assert np.max(xr) <= 1e-9
+
+
+@pytest.mark.parametrize("kind,dims,k,p,mode", [(3, (24, 24, 24), 32, 8, "hybrid"),
+                                                (4, (18, 16, 12), 16, 16, "hybrid"),
+                                                (4, (18, 16, 12), 16, 4, "global"),
+                                                (3, (20, 17, 8), 64, 16, "hybrid")])
+@pytest.mark.parametrize("nparts", [1, 2, 4])
+def test_grid_parts(ctx, monkeypatch, kind, dims, k, p, mode, nparts):
+    """k1_grid in the partitioned loop (kernels_grid.cuh): a part that is whole
+    z-planes of a constant-coefficient stencil reads its ghost-extended P as
+    a (column, x, y, plane) tensor; planes that need no ghost plane are
+    launched while the halo copies run, the one or two end planes after them.
+    Bars against the unpartitioned fast solve with the CSR K1."""
+    monkeypatch.setenv("BKG_K1_GRID", "1")
+    monkeypatch.setenv("BKG_RESIDENT", "0")
+    a = bk.stencil(kind, *dims, seed=11)
+    n = a.n()
+    b = bk.normal_block_rhs(n, k, 7)
+    cfg = bk.SubalgebraConfig(k, p, mode)
+    s = PartitionedSolver.virtual(a, cfg, nparts, ctx)
+    plane = dims[0] * dims[1]
+    tiles = -(-dims[0] // 16) * -(-dims[1] // 16) * (k // 16)
+    for i in range(nparts):
+        info = s.part_info(i)
+        r0, r1 = info["rows"]
+        if r0 % plane or r1 % plane:  # not whole planes: the CSR kernels
+            assert info["k1"] != "k1_grid"
+            continue
+        assert info["k1"] == "k1_grid"
+        nbrs = (i > 0) + (i < nparts - 1)
+        planes = (r1 - r0) // plane
+        assert info["boundary_blocks"] == tiles * min(nbrs, planes)  # one plane per neighbour
+        assert (info["interior_blocks"] > 0) == (planes > nbrs)
+    s.set_rhs(b)
+    rep, _ = s.run(1e-300, 30, record_history=True)
+    hist, x = s.history(rep.history_rows), s.x()
+    s.close()
+    monkeypatch.setenv("BKG_K1_GRID", "0")
+    c2 = bk.Context(0, "fast")
+    ref = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), cfg,
+                       bk.SolveOptions(tol=1e-300, max_iter=30, record_history=True), ctx=c2)
+    c2.close()
+    h1 = np.array(ref.report.defect_history)
+    assert rep.iterations == ref.report.iterations == 30
     assert np.max(np.abs(hist - h1) / h1) <= 1e-9
     xr = np.linalg.norm(x - ref.x, axis=0) / np.linalg.norm(ref.x, axis=0)
     assert np.max(xr) <= 1e-9
