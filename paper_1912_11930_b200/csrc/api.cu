@@ -718,7 +718,7 @@ bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, 
   if (ns < 2) return false;
   grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, g, ctas);
   *smem = ft.grid_smem(ns);
-  allow_smem(ft.k1_grid[st.full27 ? 1 : 0], *smem);
+  for (int v = 0; v < 4; ++v) allow_smem(ft.k1_grid[v], *smem);
   return true;
 }
 
@@ -839,6 +839,7 @@ struct bkg_solver {
     if (fast) {
       choose_k1();
       choose_resident();
+      choose_tma23();
       const bool jac = precond == BKG_PRECOND_JACOBI;
       k2fn = jac ? ft.k2_jac : ft.k2;
       pcx = jac ? 1 : (precond == BKG_PRECOND_ILU0 ? 2 : 0);
@@ -867,6 +868,73 @@ struct bkg_solver {
     unsigned char bytes[128];
   };
   std::vector<std::pair<const double*, TensorMap>> grid_maps;
+  // K2 / K3 with TMA-staged tiles (kernels_tma.cuh): picked for the M = I
+  // deferred-X loop of large systems (BKG_TMA23=0/1 forces it off/on); one 2-D
+  // tensor map per (block vector, tile rows)
+  bool tma23 = false;
+  int gtma = 1;
+  struct Map2d {
+    const double* ptr;
+    int rows;
+    TensorMap tm;
+  };
+  std::vector<Map2d> maps2d;
+  const unsigned char* map2d(const double* ptr, int rows) {
+    for (auto& e : maps2d)
+      if (e.ptr == ptr && e.rows == rows) return e.tm.bytes;
+    maps2d.push_back(Map2d{ptr, rows, TensorMap{}});
+    tile_tensor_map(ptr, k, n, rows, maps2d.back().tm.bytes);
+    return maps2d.back().tm.bytes;
+  }
+  void choose_tma23() {
+    tma23 = false;
+    const char* env = std::getenv("BKG_TMA23");
+    if (!fast || !ft.k2_tma || precond != BKG_PRECOND_IDENTITY || !BKG_DEFER_X) return;
+    if (env && env[0] == '0') return;
+    if (!env && (!ft.tma23_auto || n < (1 << 16))) return;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    if (ft.tma_smem > std::min(optin, 227 * 1024)) return;
+    allow_smem(ft.k2_tma, ft.tma_smem);
+    allow_smem(ft.k3_tma[0], ft.tma_smem);
+    allow_smem(ft.k3_tma[1], ft.tma_smem);
+    gtma = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->sm_count, (n + 31) / 32));
+    tma23 = true;
+    maps2d.clear();
+    maps2d.reserve(16);
+  }
+  // K2 / K3 launches of the fused M = I loop (register-operand or TMA kernels)
+  void launch_k2(IterArgs& a) {
+    if (tma23) {
+      alignas(64) unsigned char maps[5 * 128] = {};
+      std::memcpy(maps, map2d(a.Q, 32), 128);
+      std::memcpy(maps + 128, map2d(a.R, 32), 128);
+      void* args[] = {&a, maps};
+      launch(ctx, ft.k2_tma, gtma, kThreads, ft.tma_smem, args);
+      return;
+    }
+    void* args[] = {&a};
+    launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
+  }
+  void launch_k3(IterArgs& a, const void* k3) {
+    if (tma23 && defer && a.Pn != a.P) {
+      const bool flush = a.Pold != nullptr;
+      const int tr = flush ? 16 : 32;
+      alignas(64) unsigned char maps[5 * 128] = {};
+      std::memcpy(maps, map2d(a.P, tr), 128);
+      std::memcpy(maps + 128, map2d(a.R, tr), 128);
+      std::memcpy(maps + 256, map2d(a.Pn, tr), 128);
+      if (flush) {
+        std::memcpy(maps + 384, map2d(a.X, tr), 128);
+        std::memcpy(maps + 512, map2d(a.Pold, tr), 128);
+      }
+      void* args[] = {&a, maps};
+      launch(ctx, ft.k3_tma[flush ? 1 : 0], gtma, kThreads, ft.tma_smem, args);
+      return;
+    }
+    void* args[] = {&a};
+    launch(ctx, k3, g3, kThreads, ft.smem_iter, args);
+  }
   int k1_threads = kThreads;  // k1_stage runs 16 warps per CTA
   int stage_ns = 0;  // k1_stage ring depth
 
@@ -951,7 +1019,7 @@ struct bkg_solver {
     int smem = 0;
     if (use_grid(ctx, A, ft, k, &grid_args, &g1, &smem)) {
       k1_kind = 4;
-      ft.k1 = ft.k1_grid[A->gridst.full27 ? 1 : 0];
+      ft.k1 = ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
       ft.smem_k1 = smem;
       k1_threads = kGridThreads;
       grid_maps.clear();
@@ -1121,9 +1189,9 @@ struct bkg_solver {
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[0], ctx->stream));
       launch_k1(a);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[1], ctx->stream));
-      launch(ctx, k2fn, g2, kThreads, ft.smem_iter, args);
+      launch_k2(a);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[2], ctx->stream));
-      launch(ctx, k3, g3, kThreads, ft.smem_iter, args);
+      launch_k3(a, k3);
       if (ev) BKG_CUDA_CHECK(cudaEventRecord(ev[3], ctx->stream));
       return;
     }
@@ -1596,7 +1664,10 @@ int bkg_bdot(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, const d
     if (n == 0) {
       std::fill(out, out + cs, 0.0);
     } else {
-      DevBuf<double> dx(n * k), dy(n * k), dout(cs);
+      DevBuf<double>&dx = ctx->kbuf[0], &dy = ctx->kbuf[1], &dout = ctx->kbuf[2];
+      dx.ensure(n * k);
+      dy.ensure(n * k);
+      dout.ensure(cs);
       h2d(ctx, dx.ptr, x, n * k);
       h2d(ctx, dy.ptr, y, n * k);
       dev_gram(ctx, (int64_t)n, (int)k, (int)p, global, dx.ptr, dy.ptr, dout.ptr);
@@ -1616,7 +1687,10 @@ int bkg_baxpy(bkg_ctx* ctx, uint64_t n, uint64_t k, uint64_t p, int mode, double
     const int nblk = global ? 1 : (int)(k / p);
     const size_t cs = (size_t)nblk * p * p;
     if (n > 0) {
-      DevBuf<double> dx(n * k), dy(n * k), dg(cs);
+      DevBuf<double>&dx = ctx->kbuf[0], &dy = ctx->kbuf[1], &dg = ctx->kbuf[2];
+      dx.ensure(n * k);
+      dy.ensure(n * k);
+      dg.ensure(cs);
       h2d(ctx, dx.ptr, x, n * k);
       h2d(ctx, dy.ptr, y, n * k);
       h2d(ctx, dg.ptr, gamma, cs);
@@ -1635,7 +1709,9 @@ int bkg_bop(bkg_ctx* ctx, const bkg_matrix* a, uint64_t k, const double* x, doub
     BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
     activate(ctx);
     const uint64_t n = a->n;
-    DevBuf<double> dx(n * k), dy(n * k);
+    DevBuf<double>&dx = ctx->kbuf[0], &dy = ctx->kbuf[1];
+    dx.ensure(n * k);
+    dy.ensure(n * k);
     h2d(ctx, dx.ptr, x, n * k);
     dev_spmm(ctx, a, (int)k, dx.ptr, dy.ptr);
     d2h(ctx, y, dy.ptr, n * k);
@@ -1654,8 +1730,12 @@ int bkg_bsolve(bkg_ctx* ctx, uint64_t k, uint64_t p, int mode, const double* gam
     const bool global = mode == BKG_GLOBAL && p != k;
     const int nblk = global ? 1 : (int)(k / p);
     const size_t cs = (size_t)nblk * p * p;
-    DevBuf<double> dg(cs), dd(cs), dout(cs);
-    DevBuf<int> dst(1);
+    DevBuf<double>&dg = ctx->kbuf[0], &dd = ctx->kbuf[1], &dout = ctx->kbuf[2];
+    DevBuf<int>& dst = ctx->kstatus;
+    dg.ensure(cs);
+    dd.ensure(cs);
+    dout.ensure(cs);
+    dst.ensure(1);
     h2d(ctx, dg.ptr, gamma, cs);
     h2d(ctx, dd.ptr, delta, cs);
     dev_bsolve(ctx, nblk, (int)p, dg.ptr, dd.ptr, dout.ptr, dst.ptr);
@@ -1682,7 +1762,9 @@ int bkg_column_norms(bkg_ctx* ctx, uint64_t n, uint64_t k, const double* x, doub
       std::fill(out, out + k, 0.0);
       return;
     }
-    DevBuf<double> dx(n * k), dout(k);
+    DevBuf<double>&dx = ctx->kbuf[0], &dout = ctx->kbuf[2];
+    dx.ensure(n * k);
+    dout.ensure(k);
     h2d(ctx, dx.ptr, x, n * k);
     dev_norms(ctx, (int64_t)n, (int)k, dx.ptr, dout.ptr);
     d2h(ctx, out, dout.ptr, k);
@@ -1697,7 +1779,9 @@ int bkg_precond_apply(bkg_ctx* ctx, const bkg_matrix* a, int precond, uint64_t k
     BKG_REQUIRE(k > 0, BKG_CONFIG, "BlockVector: column count must be positive");
     activate(ctx);
     const uint64_t n = a->n;
-    DevBuf<double> dr(n * k), dz(n * k);
+    DevBuf<double>&dr = ctx->kbuf[0], &dz = ctx->kbuf[1];
+    dr.ensure(n * k);
+    dz.ensure(n * k);
     h2d(ctx, dr.ptr, r, n * k);
     const uint64_t f = precond_apply_dev(ctx, const_cast<bkg_matrix*>(a), precond, (int)k,
                                          dr.ptr, dz.ptr, nullptr);

@@ -207,6 +207,11 @@ struct bkg_ctx {
   bkg::DevBuf<double> scratch;
   bkg::DevBuf<char> ctrl;  // one bkg::Ctrl for standalone kernels
   bkg::DevBuf<char> upload_tmp;  // staging for size_t column uploads
+  // operands of the kernel-level entry points (bkg_bdot, bkg_baxpy, bkg_bop,
+  // bkg_bsolve, bkg_column_norms, bkg_precond_apply): grow-only, so a loop of
+  // such calls does not pay a synchronising cudaMalloc + cudaFree per call
+  bkg::DevBuf<double> kbuf[3];
+  bkg::DevBuf<int> kstatus;
   // CSR buffers of the last destroyed matrix, reused by the next upload
   // (stream-ordered; saves a synchronising cudaFree + cudaMalloc per call)
   bkg::DevBuf<int64_t> spare_rowptr;

@@ -10,6 +10,7 @@
 #include "kernels_resident.cuh"
 #include "kernels_stage.cuh"
 #include "kernels_grid.cuh"
+#include "kernels_tma.cuh"
 
 // K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
 #ifndef BKG_K1_IMPL
@@ -89,10 +90,17 @@ struct FastTable {
   int stage_R0 = 0;
   int (*stage_smem)(int R, int cap, int wmax, int ns) = nullptr;
   // k1_grid alternative (constant-coefficient grid stencils from TMA-tiled
-  // planes, kernels_grid.cuh): [0] 7-point, [1] 27-point
-  const void* k1_grid[2] = {nullptr, nullptr};
+  // planes, kernels_grid.cuh): [0] 7-point, [1] 27-point; [+2] with the
+  // lockstep pacing compiled in (long launches)
+  const void* k1_grid[4] = {nullptr, nullptr, nullptr, nullptr};
   bool grid_auto = false;  // the solver may pick it without BKG_K1_GRID=1
   int (*grid_smem)(int ns) = nullptr;
+  // K2 / K3 with TMA-staged operand tiles (kernels_tma.cuh; M = I loop with
+  // the deferred X update): k3_tma[0] skip, [1] flush
+  const void* k2_tma = nullptr;
+  const void* k3_tma[2] = {nullptr, nullptr};
+  int tma_smem = 0;
+  bool tma23_auto = false;  // the solver may pick them without BKG_TMA23=1
   // latency path for small systems (kernels_resident.cuh): the whole loop as
   // one cooperative kernel with 1 or 4 row passes per CTA
   const void* resident[2] = {nullptr, nullptr};
@@ -133,11 +141,17 @@ void fill_table(FastTable* t) {
     t->stage_R0 = StageLayout<K, P, W>::R0;
     t->stage_smem = &k1_stage_smem<K, P, W, G>;
     if constexpr (K % kGridW == 0 && K <= 128) {
-      t->k1_grid[0] = (const void*)&k1_grid<K, P, G, false>;
-      t->k1_grid[1] = (const void*)&k1_grid<K, P, G, true>;
+      t->k1_grid[0] = (const void*)&k1_grid<K, P, G, false, false>;
+      t->k1_grid[1] = (const void*)&k1_grid<K, P, G, true, false>;
+      t->k1_grid[2] = (const void*)&k1_grid<K, P, G, false, true>;
+      t->k1_grid[3] = (const void*)&k1_grid<K, P, G, true, true>;
       t->grid_smem = &k1_grid_smem<K, P, G>;
       // B200: C5 K1 6.93 -> 3.07 ms, C2 0.354 -> 0.207, C4 1.87 -> 0.44
       t->grid_auto = true;
+      t->k2_tma = (const void*)&k2_tma<K, P, G>;
+      t->k3_tma[0] = (const void*)&k3_tma<K, P, G, 1>;
+      t->k3_tma[1] = (const void*)&k3_tma<K, P, G, 2>;
+      t->tma_smem = k23_tma_smem<K, P, G>();
       if (32 * 8 * (K / kGridW) > t->e_iter) t->e_iter = 32 * 8 * (K / kGridW);
     }
   } else if constexpr (K % 8 == 0 && P <= 16) {  // warp-tile SpMM + DMMA Gram

@@ -225,11 +225,12 @@ void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool low
 
 // TMA tensor map of a row-major n x K block vector seen as (column, x, y, z),
 // box = one 16-column plane tile with its halo, 128-byte swizzle, zero fill.
-void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) {
-  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+namespace {
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn tensor_map_encoder() {
   static EncodeFn encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -239,6 +240,29 @@ void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) 
                 "cuTensorMapEncodeTiled is not available from the driver");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
+  return encode;
+}
+}  // namespace
+
+// 2-D tensor map of a row-major n x K block vector (column, row), box = one
+// 16-column x `rows`-row tile, 128-byte swizzle; rows past n read as zero and
+// are not written (kernels_tma.cuh).
+void tile_tensor_map(const double* P, int K, int64_t n, int rows, void* out) {
+  EncodeFn encode = tensor_map_encoder();
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 8};
+  const cuuint32_t box[2] = {kGridW, (cuuint32_t)rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             2, const_cast<double*>(P), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
+              "cuTensorMapEncodeTiled (2-D) failed (" + std::to_string((int)rc) + ")");
+}
+
+void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) {
+  EncodeFn encode = tensor_map_encoder();
   const cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
   const cuuint64_t strides[3] = {(cuuint64_t)K * 8, (cuuint64_t)K * 8 * nx,
                                  (cuuint64_t)K * 8 * nx * ny};

@@ -33,6 +33,8 @@ void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool low
                     int zoff, GridArgs* g, int* ctas);
 void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out);
 int grid_ring_depth(const FastTable& ft, int K, int per_cta);
+// 2-D tensor map of a row-major n x K block vector, box = 16 columns x `rows` rows
+void tile_tensor_map(const double* P, int K, int64_t n, int rows, void* out);
 // generate.cu: device-side problem generation
 void dev_generate_rhs(bkg_ctx* c, int normal, int64_t n, int k, uint64_t seed, double* dst,
                       int64_t row0 = 0);

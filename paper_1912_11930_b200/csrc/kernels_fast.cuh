@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
 // solve and the stop test); unless the solve stopped: P = Z + P beta in
 // place (solver.hpp:186-190) and rho_prev' = <<P', R>> for the next K1.
 template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
-__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
+__device__ __forceinline__ void k3_update_xp_body(const IterArgs& a) {
   using L = Layout<K, P, CPT>;
   using S = FastSmem<K, P, CPT, GLOBAL>;
   // XM: deferred X update, see kernels_mma.cuh k3_mma; the skip launch
@@ -629,6 +629,10 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp
     if (XM == 2) a.ctrl->xold = 0;
     a.ctrl->xpending = 0;
   }
+}
+template <int K, int P, int CPT, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
+__global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k3_update_xp(IterArgs a) {
+  k3_update_xp_body<K, P, CPT, GLOBAL, JAC, ZS, XM>(a);
 }
 
 // ------------------------------------------------------- K2 (ILU(0)) ---

@@ -66,10 +66,6 @@ __host__ __device__ constexpr int grid_gy(int q) { return BKG_GRID_ARR ? (q >> 1
 constexpr int kGridWinX = BKG_GRID_ARR ? 4 : 12;  // window of a lane's four points + halo
 constexpr int kGridWinY = BKG_GRID_ARR ? 4 : 3;
 
-#ifndef BKG_GRID_PACE
-#define BKG_GRID_PACE 1  // 0: compile the lockstep pacing out (tuning)
-#endif
-
 struct GridArgs {
   int nx, ny, nz;
   int tx, ty;       // tiles per axis
@@ -127,7 +123,9 @@ __device__ void gather_gram_grid(const double* red, double* blocks) {
   }
 }
 
-template <int K, int P, bool GLOBAL, bool FULL27>
+// PACE: the lockstep pacing compiled in (GridArgs::sync_every > 0 launches;
+// its live state costs the 27-point loop 14% when merely present).
+template <int K, int P, bool GLOBAL, bool FULL27, bool PACE>
 __global__ void __launch_bounds__(kGridThreads, 1)
     k1_grid(IterArgs a, GridArgs g, const __grid_constant__ CUtensorMap tmP) {
   using S = FastSmem<K, P, 1, GLOBAL>;
@@ -190,7 +188,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   // nobody waits for it again.
   unsigned long long* gsync = &a.ctrl->grid_sync;
   auto pace = [&](uint32_t jn) {
-    if (!BKG_GRID_PACE) return;
+    if constexpr (!PACE) return;
     if (g.sync_every <= 0 || jn % (uint32_t)g.sync_every != 0) return;
     const long long seg = jn / (uint32_t)g.sync_every;
     atomicAdd(gsync, 1ull);
@@ -203,7 +201,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
       if (clock64() - t0 > (1ll << 21)) break;  // ~1 ms: never a correctness dependency
   };
   auto issued_last = [&](const Cursor& c) {  // c was this CTA's final copy
-    if (BKG_GRID_PACE && g.sync_every > 0 && c.i + 1 >= nmine && c.t >= c.z1) atomicAdd(gsync, 1ull << 40);
+    if (PACE && g.sync_every > 0 && c.i + 1 >= nmine && c.t >= c.z1) atomicAdd(gsync, 1ull << 40);
   };
   Cursor ahead;  // the copy NS steps ahead of the plane being consumed
   cur_start(ahead, 0);
@@ -349,7 +347,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   double* ws = alpha + 3 * S::CS;
   gather_gram_grid<K, P, GLOBAL>(red, alpha);
   __syncthreads();
-  if (threadIdx.x == 0) *gsync = 0;  // every CTA is past its loop: ready for the next launch
+  if (PACE && threadIdx.x == 0) *gsync = 0;  // every CTA is past its loop: ready for the next launch
   if (a.dist) {  // row-partitioned solver: publish this part's alpha (psolver.cu)
     for (int i = threadIdx.x; i < S::CS; i += kGridThreads)
       a.red1[i] = (a.dist_acc ? a.red1[i] : 0.0) + alpha[i];

@@ -140,6 +140,22 @@ template <int P>
 constexpr int k2_unroll() {
   return P <= 8 ? BKG_K2_U8 : 1;
 }
+// L2 bulk prefetch distance of K2 / K3 in warp steps (0: off): the warp that
+// owns column group 0 of a row block asks the copy engine to pull the whole
+// 8-row block (8 K doubles, contiguous) of every operand stream BKG_MMA_PF
+// steps ahead into L2 (cp.async.bulk.prefetch.L2: no register, no L1 miss
+// slot), so the fragment loads that follow find their lines in L2.
+#ifndef BKG_MMA_PF
+#define BKG_MMA_PF 0
+#endif
+__device__ __forceinline__ void mma_prefetch_block(const double* base, int64_t rb, int64_t nrb,
+                                                   int64_t n, int K) {
+  if (rb < nrb && rb * 8 + 8 <= n)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + rb * 8 * K),
+                 "r"((uint32_t)(8 * K * 8))
+                 : "memory");
+}
+
 template <int P, int KERNEL>
 constexpr int mma_minb() {
   return P <= 8 ? (KERNEL == 2 ? BKG_K2_MINB8 : BKG_K3_MINB8) : (KERNEL == 2 ? 3 : 2);
@@ -169,6 +185,16 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
   for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
        rb0 += U * wstride) {
     double qa[U][L::KC], rc[U][L::NT][2], dt[U][2];
+    if constexpr (BKG_MMA_PF > 0) {
+      if (g == 0 && lane == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t rbp = rb0 + (BKG_MMA_PF * U + u) * wstride;
+          mma_prefetch_block(a.Q, rbp, nrb, a.n, K);
+          mma_prefetch_block(a.R, rbp, nrb, a.n, K);
+        }
+      }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t rb = rb0 + u * wstride;
@@ -265,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
 // 2 = flush: X += Pold lambda_old + P lambda in one pass.  X is then read and
 // written every other iteration (K3 traffic 5nk -> 3nk / 6nk alternating).
 template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
-__global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
+__device__ __forceinline__ void k3_mma_body(const IterArgs& a) {
   using L = MmaLayout<K, P, GLOBAL>;
   using S = FastSmem<K, P, 1, GLOBAL>;
   const bool cur = *reinterpret_cast<const volatile int32_t*>(&a.ctrl->xpending) != 0;
@@ -296,6 +322,19 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
   for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
        rb0 += U * wstride) {
     double pa[U][L::KC], po[U][L::KC], xc[U][L::NT][2], pn[U][L::NT][2], zz[U][L::NT][2];
+    if constexpr (BKG_MMA_PF > 0) {
+      if (g == 0 && lane == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t rbp = rb0 + (BKG_MMA_PF * U + u) * wstride;
+          if (cur) mma_prefetch_block(a.P, rbp, nrb, a.n, K);
+          if (upd) mma_prefetch_block(a.R, rbp, nrb, a.n, K);
+          if (dox) mma_prefetch_block(a.X, rbp, nrb, a.n, K);
+          if constexpr (XM == 2)
+            if (old) mma_prefetch_block(a.Pold, rbp, nrb, a.n, K);
+        }
+      }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t rb = rb0 + u * wstride;
@@ -396,6 +435,10 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs 
     if (XM == 2) a.ctrl->xold = 0;
     a.ctrl->xpending = 0;
   }
+}
+template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
+__global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
+  k3_mma_body<K, P, GLOBAL, JAC, ZS, XM>(a);
 }
 
 }  // namespace bkg

@@ -342,9 +342,9 @@ struct bkg_psolver {
     const int ns = grid_ring_depth(ft, k, std::min(optin, 227 * 1024));
     if (ns < 2) return false;
     pt.k1_kind = 4;
-    pt.k1 = ft.k1_grid[st.full27 ? 1 : 0];
+    pt.k1 = ft.k1_grid[st.full27 ? 1 : 0];  // + 2: paced (interior launch, chosen per launch)
     pt.smem_k1 = ft.grid_smem(ns);
-    allow_smem(pt.k1, pt.smem_k1);
+    for (int v = 0; v < 4; ++v) allow_smem(ft.k1_grid[v], pt.smem_k1);
     const int zoff = lower ? 1 : 0;
     const int zb = lower ? 1 : 0, ze = upper ? st.nz - 1 : st.nz;
     const char* hs = std::getenv("BKG_HALO_SMS");
@@ -574,7 +574,8 @@ struct bkg_psolver {
       GridArgs ga = interior ? pt.ga_in : pt.ga_bd;
       const int cur = a.P == pt.P[1] ? 1 : 0;
       void* gargs[] = {&a, &ga, pt.tmap[cur].bytes};
-      launch(ctx, pt.k1, interior ? pt.g1i : pt.g1b, kGridThreads, pt.smem_k1, gargs);
+      const void* fn = ft.k1_grid[(pt.gst.full27 ? 1 : 0) + (ga.sync_every > 0 ? 2 : 0)];
+      launch(ctx, fn, interior ? pt.g1i : pt.g1b, kGridThreads, pt.smem_k1, gargs);
       return;
     }
     void* args[] = {&a};

@@ -13,6 +13,8 @@ import sys
 
 
 def ncu_csv(rep, page):
+    if not rep.endswith(".ncu-rep"):  # CSV pages exported on the GPU box: PREFIX.raw.csv, PREFIX.details.csv
+        return list(csv.reader(open(f"{rep}.{page}.csv")))
     out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv"], capture_output=True,
                          text=True).stdout
     return list(csv.reader(io.StringIO(out)))
