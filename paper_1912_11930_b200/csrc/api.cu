@@ -691,12 +691,12 @@ bool bkg::use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K,
 // latency kernels win).  Out: the plan, the persistent grid, dynamic smem.
 // Ring depth of k1_grid: BKG_GRID_NS, else 3 (B200 sweeps: deeper
 // rings let the CTAs drift apart and lose the halo rows in L2); 0: no fit.
+// K < 0: the variable-coefficient stage (operand box + DIA tiles).
 int bkg::grid_ring_depth(const FastTable& ft, int K, int per_cta) {
-  (void)K;
   const char* en = std::getenv("BKG_GRID_NS");
   int ns = en ? std::max(2, std::atoi(en)) : 3;
-  while (ns > 2 && ft.grid_smem(ns) > per_cta) --ns;
-  return ft.grid_smem(ns) > per_cta ? 0 : ns;
+  while (ns > 2 && ft.grid_smem(ns, K < 0) > per_cta) --ns;
+  return ft.grid_smem(ns, K < 0) > per_cta ? 0 : ns;
 }
 
 bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g,
@@ -710,16 +710,24 @@ bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, 
   if (!env && ((st_env && st_env[0] == '1') || (ln_env && ln_env[0] == '1')))
     return false;  // an explicit request for another K1 wins over the default
   const GridStencil& st = grid_stencil(c, A);
-  if (!st.ok) return false;
+  if (!st.ok && !st.var) return false;
   int optin = 0;
   BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const int per_cta = std::min(optin, 227 * 1024);
-  const int ns = grid_ring_depth(ft, K, per_cta);
+  const int ns = grid_ring_depth(ft, st.var ? -K : K, per_cta);
   if (ns < 2) return false;
-  grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, g, ctas);
-  *smem = ft.grid_smem(ns);
-  for (int v = 0; v < 4; ++v) allow_smem(ft.k1_grid[v], *smem);
+  grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, st.nz, g, ctas);
+  *smem = ft.grid_smem(ns, st.var);
+  for (int v = 0; v < 6; ++v) allow_smem(ft.k1_grid[v], *smem);
   return true;
+}
+
+// Byte offset between the starts of a solver's block vectors inside their
+// allocations (BKG_VEC_SKEW, a multiple of 256; tuning).
+static size_t vec_skew() {
+  const char* e = std::getenv("BKG_VEC_SKEW");
+  const long long v = e ? std::atoll(e) : 0;
+  return v > 0 ? (size_t)(v / 256 * 256) : 0;
 }
 
 // =========================================================== solver =====
@@ -820,12 +828,14 @@ struct bkg_solver {
     // (reference-order) kernel sequence with Z = M^-1 R on device
     fast = use_fast(c, k, p, global, &ft) && fused_precond(precond);
     const size_t nk = (size_t)n * k;
-    B.alloc(nk);
-    X.alloc(nk);
-    R.alloc(nk);
-    Q.alloc(nk);
-    Pb.alloc(nk);
-    if (!fast || pc == BKG_PRECOND_ILU0) Zb.alloc(nk);
+    // each block vector starts i * vec_skew bytes into its allocation (i = 0..6)
+    const size_t sk = vec_skew();
+    B.alloc_skewed(nk, 0 * sk);
+    X.alloc_skewed(nk, 1 * sk);
+    R.alloc_skewed(nk, 2 * sk);
+    Q.alloc_skewed(nk, 3 * sk);
+    Pb.alloc_skewed(nk, 4 * sk);
+    if (!fast || pc == BKG_PRECOND_ILU0) Zb.alloc_skewed(nk, 6 * sk);
     P = Pb.ptr;
     Z = Zb.ptr;
     coef.alloc((size_t)6 * cs);
@@ -844,7 +854,7 @@ struct bkg_solver {
       k2fn = jac ? ft.k2_jac : ft.k2;
       pcx = jac ? 1 : (precond == BKG_PRECOND_ILU0 ? 2 : 0);
       k3fn = ft.k3x[pcx][0];
-      if (BKG_DEFER_X) Pb2.alloc(nk);
+      if (BKG_DEFER_X) Pb2.alloc_skewed(nk, 5 * sk);
       g2 = occupancy_grid(c, k2fn, ft.smem_iter, n, ft.rpc_k2);
       g3 = std::min(occupancy_grid(c, k3fn, ft.smem_iter, n, ft.rpc_k3),
                     occupancy_grid(c, ft.k3x[pcx][2], ft.smem_iter, n, ft.rpc_k3));
@@ -867,7 +877,10 @@ struct bkg_solver {
   struct alignas(64) TensorMap {
     unsigned char bytes[128];
   };
-  std::vector<std::pair<const double*, TensorMap>> grid_maps;
+  struct alignas(64) GridMapSet {  // GridMaps of kernels_grid.cuh: p, v5, v1
+    unsigned char bytes[3 * 128];
+  };
+  std::vector<std::pair<const double*, GridMapSet>> grid_maps;
   // K2 / K3 with TMA-staged tiles (kernels_tma.cuh): picked for the M = I
   // deferred-X loop of large systems (BKG_TMA23=0/1 forces it off/on); one 2-D
   // tensor map per (block vector, tile rows)
@@ -1019,7 +1032,9 @@ struct bkg_solver {
     int smem = 0;
     if (use_grid(ctx, A, ft, k, &grid_args, &g1, &smem)) {
       k1_kind = 4;
-      ft.k1 = ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
+      ft.k1 = A->gridst.var
+                  ? ft.k1_grid[4 + (grid_args.sync_every > 0 ? 1 : 0)]
+                  : ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
       ft.smem_k1 = smem;
       k1_threads = kGridThreads;
       grid_maps.clear();
@@ -1062,13 +1077,18 @@ struct bkg_solver {
   // (the deferred-X loop alternates two P buffers) as extra parameters.
   void launch_k1(IterArgs& a) {
     if (k1_kind == 4) {
-      TensorMap* tm = nullptr;
+      GridMapSet* tm = nullptr;
       for (auto& e : grid_maps)
         if (e.first == a.P) tm = &e.second;
       if (!tm) {
-        grid_maps.emplace_back(a.P, TensorMap{});
+        const GridStencil& gs = A->gridst;
+        grid_maps.emplace_back(a.P, GridMapSet{});
         tm = &grid_maps.back().second;
-        grid_tensor_map(a.P, k, A->gridst.nx, A->gridst.ny, A->gridst.nz, tm->bytes);
+        grid_tensor_map(a.P, k, gs.nx, gs.ny, gs.nz, tm->bytes);
+        if (gs.var) {
+          grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 5, tm->bytes + 128);
+          grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 1, tm->bytes + 256);
+        }
       }
       void* args[] = {&a, &grid_args, tm->bytes};
       launch(ctx, ft.k1, g1, k1_threads, ft.smem_k1, args);
@@ -1956,7 +1976,9 @@ int bkg_solver_kernel_bytes(const bkg_solver* s, double* out) {
     if (s->fast) {
       // K1: read P (once, neighbours via L1/L2); write Q; the CSR stream --
       // which k1_grid never reads (constant stencil): not counted for it
-      out[0] = 2.0 * nk8 + (s->k1_kind == 4 ? 0.0 : csr);
+      out[0] = 2.0 * nk8 + (s->k1_kind != 4 ? csr
+                            : s->A->gridst.var ? 56.0 * (double)s->n  // the DIA tiles
+                                               : 0.0);
       const double jac = s->precond == BKG_PRECOND_JACOBI ? 8.0 * (double)s->n : 0.0;
       out[1] = 3.0 * nk8 + jac;  // K2: read Q, R; write R (+ D^-1 for Jacobi)
       // K3: read P, X, R; write P, X (+ D^-1); deferred X: skip launches read

@@ -52,12 +52,14 @@ template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
+  void* base = nullptr;  // the allocation (ptr = base + a skew, alloc_skewed)
   DevBuf() = default;
   explicit DevBuf(size_t n) { alloc(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) {
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count), base(o.base) {
     o.ptr = nullptr;
+    o.base = nullptr;
     o.count = 0;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
@@ -65,24 +67,33 @@ struct DevBuf {
       release();
       ptr = o.ptr;
       count = o.count;
+      base = o.base;
       o.ptr = nullptr;
+      o.base = nullptr;
       o.count = 0;
     }
     return *this;
   }
   ~DevBuf() { release(); }
-  void alloc(size_t n) {
+  void alloc(size_t n) { alloc_skewed(n, 0); }
+  // n elements starting skew_bytes (a multiple of 256) into the allocation:
+  // block vectors whose size is a power of two would otherwise sit exactly
+  // 2^m bytes apart and send the same row of every stream of a kernel to the
+  // same L2 slice / DRAM bank (vec_skew, api.cu)
+  void alloc_skewed(size_t n, size_t skew_bytes) {
     release();
     if (n == 0) return;
-    BKG_CUDA_CHECK(cudaMalloc(&ptr, n * sizeof(T)));
+    BKG_CUDA_CHECK(cudaMalloc(&base, n * sizeof(T) + skew_bytes));
+    ptr = reinterpret_cast<T*>(static_cast<char*>(base) + skew_bytes);
     count = n;
   }
   void ensure(size_t n) {
     if (n > count) alloc(n);
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (base) cudaFree(base);
     ptr = nullptr;
+    base = nullptr;
     count = 0;
   }
   size_t bytes() const { return count * sizeof(T); }
@@ -191,6 +202,11 @@ struct GridStencil {
   int zs = 0, nzg = 0;         // first global plane of the rows, planes of the global grid
   bool full27 = false;  // entries off the 7-point star
   double c[3][9] = {};
+  // Variable coefficients (ok stays false): the pattern is a 5 / 7-point star
+  // on the grid and dia holds its DIA copy V[slot * n + row], slots dz-1 |
+  // dy-1 dx-1 0 dx+1 dy+1 | dz+1, zero where a row has no such entry.
+  bool var = false;
+  DevBuf<double> dia;
 };
 
 }  // namespace bkg

@@ -91,10 +91,11 @@ struct FastTable {
   int (*stage_smem)(int R, int cap, int wmax, int ns) = nullptr;
   // k1_grid alternative (constant-coefficient grid stencils from TMA-tiled
   // planes, kernels_grid.cuh): [0] 7-point, [1] 27-point; [+2] with the
-  // lockstep pacing compiled in (long launches)
-  const void* k1_grid[4] = {nullptr, nullptr, nullptr, nullptr};
+  // lockstep pacing compiled in (long launches); [4], [5]: 5 / 7-point with
+  // variable coefficients (DIA tiles), unpaced / paced
+  const void* k1_grid[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool grid_auto = false;  // the solver may pick it without BKG_K1_GRID=1
-  int (*grid_smem)(int ns) = nullptr;
+  int (*grid_smem)(int ns, bool var) = nullptr;
   // K2 / K3 with TMA-staged operand tiles (kernels_tma.cuh; M = I loop with
   // the deferred X update): k3_tma[0] skip, [1] flush
   const void* k2_tma = nullptr;
@@ -145,6 +146,8 @@ void fill_table(FastTable* t) {
       t->k1_grid[1] = (const void*)&k1_grid<K, P, G, true, false>;
       t->k1_grid[2] = (const void*)&k1_grid<K, P, G, false, true>;
       t->k1_grid[3] = (const void*)&k1_grid<K, P, G, true, true>;
+      t->k1_grid[4] = (const void*)&k1_grid<K, P, G, false, false, true>;
+      t->k1_grid[5] = (const void*)&k1_grid<K, P, G, false, true, true>;
       t->grid_smem = &k1_grid_smem<K, P, G>;
       // B200: C5 K1 6.93 -> 3.07 ms, C2 0.354 -> 0.207, C4 1.87 -> 0.44
       t->grid_auto = true;

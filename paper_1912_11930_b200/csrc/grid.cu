@@ -64,6 +64,37 @@ __global__ void k_grid_check(int64_t n, int64_t r0, int nx, int ny, int nz,
   }
 }
 
+// Variable coefficients: every entry must sit on the 5 / 7-point star of its
+// row (columns ascending); its value goes to V[slot * n + row] (V zeroed before).
+__global__ void k_grid_dia(int64_t n, int nx, int ny, int nz, const int64_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                           double* __restrict__ V, int* __restrict__ bad) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(r % nx), y = (int)((r / nx) % ny), z = (int)(r / ((int64_t)nx * ny));
+    int64_t prev = -1;
+    bool ok = true;
+    for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+      const int64_t c = cols[e];
+      if (c <= prev || c < 0 || c >= n) {
+        ok = false;
+        break;
+      }
+      prev = c;
+      const int dx = (int)(c % nx) - x, dy = (int)((c / nx) % ny) - y,
+                dz = (int)(c / ((int64_t)nx * ny)) - z;
+      const int ad = (dx < 0 ? -dx : dx) + (dy < 0 ? -dy : dy) + (dz < 0 ? -dz : dz);
+      if (ad > 1) {
+        ok = false;
+        break;
+      }
+      const int slot = dz ? (dz < 0 ? 0 : 6) : dy ? (dy < 0 ? 1 : 5) : dx ? (dx < 0 ? 2 : 4) : 3;
+      V[(int64_t)slot * n + r] = vals[e];
+    }
+    if (!ok) *bad = 1;
+  }
+}
+
 }  // namespace
 
 // Rows [r0, r0 + n) of a global matrix of `nglobal` rows, stored with columns
@@ -82,12 +113,14 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
   const int nx = (int)grid[0], ny = (int)grid[1];
   const int64_t plane = (int64_t)nx * ny;
   if (r0 % plane != 0 || nglobal % plane != 0 || n % plane != 0) return;  // whole planes only
-  if (nglobal / plane > (1 << 20) || nglobal / plane < 3) return;  // 3-D only
+  if (nglobal / plane > (1 << 20) || nglobal / plane == 2) return;  // 2-D (one plane) or 3-D
   const int nz = (int)(n / plane), nzg = (int)(nglobal / plane), zs = (int)(r0 / plane);
   // a row away from every face of the global grid
   int zm = nz / 2;
-  if (zs + zm < 1) zm = 1 - zs;
-  if (zs + zm > nzg - 2) zm = nzg - 2 - zs;
+  if (nzg > 1) {
+    if (zs + zm < 1) zm = 1 - zs;
+    if (zs + zm > nzg - 2) zm = nzg - 2 - zs;
+  }
   if (zm < 0 || zm >= nz) return;
   const int64_t mid = ((int64_t)zm * ny + ny / 2) * nx + nx / 2;
   int64_t rp[2];
@@ -128,13 +161,34 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
   int hbad = 1;
   d2h(c, &hbad, bad.ptr, 1);
   sync(c);
-  if (hbad) return;
-  st.ok = true;
   st.nx = nx;
   st.ny = ny;
   st.nz = nz;
   st.zs = zs;
   st.nzg = nzg;
+  if (hbad) {
+    // not one value per offset: variable coefficients on a 5 / 7-point star?
+    // (whole matrices; TMA strides need an even nx)
+    const char* ev = std::getenv("BKG_GRID_VAR");
+    if (r0 != 0 || nglobal != n || (nx & 1) || (ev && ev[0] == '0')) return;
+    st.dia.alloc((size_t)7 * n);
+    BKG_CUDA_CHECK(cudaMemsetAsync(st.dia.ptr, 0, st.dia.bytes(), c->stream));
+    BKG_CUDA_CHECK(cudaMemsetAsync(bad.ptr, 0, sizeof(int), c->stream));
+    int64_t nn = n;
+    int ax = nx, ay = ny, az = nz;
+    double* vp = st.dia.ptr;
+    int* bp = bad.ptr;
+    void* args[] = {&nn, &ax, &ay, &az, &rowptr, &cols, &vals, &vp, &bp};
+    launch(c, (const void*)&k_grid_dia, elem_grid(c, n), 256, 0, args);
+    d2h(c, &hbad, bad.ptr, 1);
+    sync(c);
+    if (hbad)
+      st.dia.release();
+    else
+      st.var = true;
+    return;
+  }
+  st.ok = true;
   for (int o = 0; o < 27; ++o) {
     st.c[o / 9][o % 9] = cf.c[o];
     const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
@@ -157,7 +211,7 @@ const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A) {
 // Rows produced: planes [zbeg, zend) of the part; zoff = the part's plane 0 in
 // the operand tensor.
 void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int zend, int zoff,
-               GridArgs* g, int* ctas) {
+               int nzt, GridArgs* g, int* ctas) {
   const int nsl = K / kGridW;
   const int nzr = zend - zbeg;
   std::memset(g, 0, sizeof(*g));
@@ -167,6 +221,8 @@ void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int
   g->zbeg = zbeg;
   g->zend = zend;
   g->zoff = zoff;
+  g->tmin = -zoff;            // planes of the operand tensor, in part coordinates
+  g->tmax = nzt - 1 - zoff;
   g->tx = (st.nx + kGridBX - 1) / kGridBX;
   g->ty = (st.ny + kGridBY - 1) / kGridBY;
   g->ns = ns;
@@ -208,9 +264,9 @@ void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int
 // The two single-plane items per (tile, slice) at the ends of a z-slab part:
 // planes 0 and nz - 1 (the rows that read the neighbours' ghost planes).
 void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool lower, bool upper,
-                    int zoff, GridArgs* g, int* ctas) {
+                    int zoff, int nzt, GridArgs* g, int* ctas) {
   const int first = lower ? 0 : st.nz - 1;
-  grid_plan(st, K, sm_count, ns, first, first + 1, zoff, g, ctas);
+  grid_plan(st, K, sm_count, ns, first, first + 1, zoff, nzt, g, ctas);
   if (lower && upper && st.nz > 1) {
     g->zend = st.nz;
     g->zstride = st.nz - 1;
@@ -259,6 +315,23 @@ void tile_tensor_map(const double* P, int K, int64_t n, int rows, void* out) {
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
               "cuTensorMapEncodeTiled (2-D) failed (" + std::to_string((int)rc) + ")");
+}
+
+// Tensor maps of the DIA copy V seen as (x, y, z, slot): boxes of one 16 x 16
+// tile x `slots` slots (5: the in-plane slots, 1: a dz slot); zero fill.
+void grid_dia_tensor_map(const double* V, int nx, int ny, int nz, int slots, void* out) {
+  EncodeFn encode = tensor_map_encoder();
+  const cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz, 7};
+  const cuuint64_t strides[3] = {(cuuint64_t)8 * nx, (cuuint64_t)8 * nx * ny,
+                                 (cuuint64_t)8 * nx * ny * nz};
+  const cuuint32_t box[4] = {kGridBX, kGridBY, 1, (cuuint32_t)slots};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult rc = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             4, const_cast<double*>(V), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
+              "cuTensorMapEncodeTiled (DIA) failed (" + std::to_string((int)rc) + ")");
 }
 
 void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) {

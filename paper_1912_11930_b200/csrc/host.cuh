@@ -28,10 +28,11 @@ const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A);
 void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
                        const double* vals, int64_t r0, int64_t nglobal, GridStencil& st);
 void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int zend, int zoff,
-               GridArgs* g, int* ctas);
+               int nzt, GridArgs* g, int* ctas);
 void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool lower, bool upper,
-                    int zoff, GridArgs* g, int* ctas);
+                    int zoff, int nzt, GridArgs* g, int* ctas);
 void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out);
+void grid_dia_tensor_map(const double* V, int nx, int ny, int nz, int slots, void* out);
 int grid_ring_depth(const FastTable& ft, int K, int per_cta);
 // 2-D tensor map of a row-major n x K block vector, box = 16 columns x `rows` rows
 void tile_tensor_map(const double* P, int K, int64_t n, int rows, void* out);

@@ -52,6 +52,17 @@ constexpr int kGridPitch = kGridBX + 2;    // box rows per tile row
 constexpr int kGridBoxRows = kGridPitch * (kGridBY + 2);
 constexpr int kGridBoxBytes = kGridBoxRows * 128;
 constexpr int kGridStageBytes = (kGridBoxBytes + 1023) / 1024 * 1024;
+// Variable coefficients (VAR): the stage also holds the tile's coefficients from
+// the DIA copy of the matrix (grid.cu: V[slot][row], slots dz-1 | dy-1 dx-1 0
+// dx+1 dy+1 | dz+1): the 5 in-plane slots of plane t, slot dz+1 of plane t-1
+// and slot dz-1 of plane t+1, 16 x 16 doubles each.
+constexpr int kGridTile = kGridBX * kGridBY;
+constexpr int kGridValBytes = 7 * kGridTile * 8;
+constexpr int kGridStageBytesVar = kGridStageBytes + kGridValBytes;
+
+struct GridMaps {  // p: the operand block vector; v5 / v1: the DIA copy, boxes of 5 / 1 slots
+  CUtensorMap p, v5, v1;
+};
 
 // Row groups of a warp (tuning, B200 sweeps in DESIGN.md §5):
 //   1  8 x 2 points: x = 8 (w & 1) + (g & 1) + 2 r, y = 2 (w >> 1) + (g >> 1)
@@ -76,6 +87,10 @@ struct GridArgs {
   // plane, psolver.cu): plane t is tensor plane t + zoff, and planes outside
   // the tensor read as zero.
   int zbeg, zend, zstride, zoff;
+  // planes that exist in the operand tensor: [tmin, tmax] (part coordinates).
+  // A plane outside is all zero: it is neither copied nor computed, and a row
+  // whose dz = +1 plane does not exist is finished by a tail step.
+  int tmin, tmax;
   int ns;           // ring depth
   // Lockstep pacing (0: off): before issuing the copy of its step j, j a
   // multiple of sync_every, a CTA waits until the grid as a whole has issued
@@ -125,9 +140,11 @@ __device__ void gather_gram_grid(const double* red, double* blocks) {
 
 // PACE: the lockstep pacing compiled in (GridArgs::sync_every > 0 launches;
 // its live state costs the 27-point loop 14% when merely present).
-template <int K, int P, bool GLOBAL, bool FULL27, bool PACE>
+template <int K, int P, bool GLOBAL, bool FULL27, bool PACE, bool VAR = false>
 __global__ void __launch_bounds__(kGridThreads, 1)
-    k1_grid(IterArgs a, GridArgs g, const __grid_constant__ CUtensorMap tmP) {
+    k1_grid(IterArgs a, GridArgs g, const __grid_constant__ GridMaps tm) {
+  static_assert(!(VAR && FULL27), "variable coefficients: 5 / 7-point stencils");
+  constexpr int STAGE = VAR ? kGridStageBytesVar : kGridStageBytes;
   using S = FastSmem<K, P, 1, GLOBAL>;
   constexpr int NSL = K / kGridW;
   constexpr int NACC = 8 * NSL;
@@ -138,7 +155,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   // SWIZZLE_128B works on shared-memory address bits: 1024-byte aligned stages
   unsigned char* smraw = smdyn + ((1024u - (smem_u32(smdyn) & 1023u)) & 1023u);
   const int NS = g.ns;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)NS * kGridStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)NS * STAGE);
   int* fin = reinterpret_cast<int*>(full + NS);  // per stage: warps done with it
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -164,23 +181,30 @@ __global__ void __launch_bounds__(kGridThreads, 1)
   // the plane copies in issue order: planes z0-1 .. z1 of item 0, 1, ...
   struct Cursor {
     int64_t i;
-    int slice, x0, y0, z1, t;
+    int slice, x0, y0, z1, t;  // z1: last plane copied for the item
   };
   auto cur_start = [&](Cursor& c, int64_t i) {
     c.i = i;
     if (i < nmine) {
-      int z0;
-      decode(i, c.slice, c.x0, c.y0, z0, c.z1);
-      c.t = z0 - 1;
+      int z0, z1;
+      decode(i, c.slice, c.x0, c.y0, z0, z1);
+      c.t = max(z0 - 1, g.tmin);
+      c.z1 = min(z1, g.tmax);
     }
   };
   auto cur_next = [&](Cursor& c) {
     if (++c.t > c.z1) cur_start(c, c.i + 1);
   };
   auto issue = [&](const Cursor& c, int s) {  // one elected lane
-    mbar_expect_tx(full + s, kGridBoxBytes);
-    tma_load_4d(smraw + (size_t)s * kGridStageBytes, &tmP, c.slice * kGridW, c.x0 - 1, c.y0 - 1,
-                c.t + g.zoff, full + s);
+    unsigned char* st = smraw + (size_t)s * STAGE;
+    mbar_expect_tx(full + s, kGridBoxBytes + (VAR ? kGridValBytes : 0));
+    tma_load_4d(st, &tm.p, c.slice * kGridW, c.x0 - 1, c.y0 - 1, c.t + g.zoff, full + s);
+    if constexpr (VAR) {  // coefficients of rows t (in-plane), t-1 (dz+1), t+1 (dz-1)
+      unsigned char* sv = st + kGridStageBytes;
+      tma_load_4d(sv, &tm.v5, c.x0, c.y0, c.t, 1, full + s);
+      tma_load_4d(sv + 5 * kGridTile * 8, &tm.v1, c.x0, c.y0, c.t - 1, 6, full + s);
+      tma_load_4d(sv + 6 * kGridTile * 8, &tm.v1, c.x0, c.y0, c.t + 1, 0, full + s);
+    }
   };
   // lockstep pacing (GridArgs::sync_every): called by the issuing lane before
   // the copy of step jn; counts this CTA into segment jn / sync_every and waits
@@ -223,6 +247,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
     // box row of group q's point: (yw + (q>>1) + 1) * pitch + 1 + xw + (q&1) + 2 r
     const int xw = BKG_GRID_ARR ? 8 * (warp & 1) : 0, yw = BKG_GRID_ARR ? 2 * (warp >> 1) : warp;
     const int ri0 = (yw + 1) * kGridPitch + 1 + xw + 2 * r;
+    const int pidx0 = yw * kGridBX + xw + 2 * r;  // tile point of group 0 (coefficient tiles)
     uint32_t j = 0;
 #pragma unroll 1
     for (int64_t i = 0; i < nmine; ++i) {
@@ -233,11 +258,33 @@ __global__ void __launch_bounds__(kGridThreads, 1)
       for (int q = 0; q < 4; ++q)
         acc_a[q][0] = acc_a[q][1] = acc_b[q][0] = acc_b[q][1] = pown[q][0] = pown[q][1] = 0.0;
       double* qbase = a.Q + slice * kGridW + 2 * m;
+      const int tlo = max(z0 - 1, g.tmin), thi = min(z1, g.tmax);
+      // rows t-1 are complete: store, Gram with their own P (the previous step's centre)
+      auto emit_rows = [&](int t, const double (&qa)[4][2]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int gx = x0 + xw + grid_gx(q) + 2 * r, gy = y0 + yw + grid_gy(q);
+          if (gx < g.nx && gy < g.ny) {
+            const int64_t row = ((int64_t)(t - 1) * g.ny + gy) * g.nx + gx;
+            *reinterpret_cast<double2*>(qbase + row * K) = make_double2(qa[q][0], qa[q][1]);
+          }
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              double d[2] = {gram[(ii * 2 + jj) * 2], gram[(ii * 2 + jj) * 2 + 1]};
+              dmma(d, pown[q][ii], qa[q][jj]);
+              gram[(ii * 2 + jj) * 2] = d[0];
+              gram[(ii * 2 + jj) * 2 + 1] = d[1];
+            }
+        }
+      };
 #pragma unroll 1
-      for (int t = z0 - 1; t <= z1; ++t, ++j) {
+      for (int t = tlo; t <= thi; ++t, ++j) {
         const int s = (int)(j % NS);
         mbar_wait(full + s, (j / NS) & 1);
-        const unsigned char* st = smraw + (size_t)s * kGridStageBytes;
+        const unsigned char* st = smraw + (size_t)s * STAGE;
+        const double* sv = reinterpret_cast<const double*>(st + kGridStageBytes) + pidx0;  // VAR
         const bool emit = t > z0;  // row t-1 belongs to this item
         // Window of this lane's four points: box rows ri0 + (py-1) pitch + (px-1),
         // px, py = 0..3.  Each operand point is read once and feeds every group
@@ -273,13 +320,23 @@ __global__ void __launch_bounds__(kGridThreads, 1)
               if (dx < -1 || dx > 1 || dy < -1 || dy > 1) continue;
               if (!(FULL27 || dx == 0 || dy == 0)) continue;
               const int o = (dy + 1) * 3 + dx + 1;
-              na[q][0] = fma(g.c[1][o], v.x, na[q][0]);
-              na[q][1] = fma(g.c[1][o], v.y, na[q][1]);
+              double c0 = g.c[1][o], cp = g.c[2][o], cm = g.c[0][o];
+              if constexpr (VAR) {  // row q's own coefficients from the DIA tiles
+                const int pq = grid_gy(q) * kGridBX + grid_gx(q);
+                const int sl = o == 1 ? 0 : o == 3 ? 1 : o == 4 ? 2 : o == 5 ? 3 : 4;
+                c0 = sv[sl * kGridTile + pq];
+                if (o == 4) {
+                  cp = sv[5 * kGridTile + pq];
+                  cm = sv[6 * kGridTile + pq];
+                }
+              }
+              na[q][0] = fma(c0, v.x, na[q][0]);
+              na[q][1] = fma(c0, v.y, na[q][1]);
               if (FULL27 || o == 4) {
-                qa[q][0] = fma(g.c[2][o], v.x, qa[q][0]);
-                qa[q][1] = fma(g.c[2][o], v.y, qa[q][1]);
-                nb[q][0] = fma(g.c[0][o], v.x, nb[q][0]);
-                nb[q][1] = fma(g.c[0][o], v.y, nb[q][1]);
+                qa[q][0] = fma(cp, v.x, qa[q][0]);
+                qa[q][1] = fma(cp, v.y, qa[q][1]);
+                nb[q][0] = fma(cm, v.x, nb[q][0]);
+                nb[q][1] = fma(cm, v.y, nb[q][1]);
               }
               if (o == 4) {  // the group's own point: next step's Gram operand
                 acc_b[q][0] = v.x;  // parked in acc_b (dead: copied into na above)
@@ -287,25 +344,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
               }
             }
           }
-        if (emit) {  // rows t-1 are complete: store, Gram with their own P (last step's centre)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int gx = x0 + xw + grid_gx(q) + 2 * r, gy = y0 + yw + grid_gy(q);
-            if (gx < g.nx && gy < g.ny) {
-              const int64_t row = ((int64_t)(t - 1) * g.ny + gy) * g.nx + gx;
-              *reinterpret_cast<double2*>(qbase + row * K) = make_double2(qa[q][0], qa[q][1]);
-            }
-#pragma unroll
-            for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-              for (int jj = 0; jj < 2; ++jj) {
-                double d[2] = {gram[(ii * 2 + jj) * 2], gram[(ii * 2 + jj) * 2 + 1]};
-                dmma(d, pown[q][ii], qa[q][jj]);
-                gram[(ii * 2 + jj) * 2] = d[0];
-                gram[(ii * 2 + jj) * 2 + 1] = d[1];
-              }
-          }
-        }
+        if (emit) emit_rows(t, qa);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           pown[q][0] = acc_b[q][0];
@@ -328,6 +367,7 @@ __global__ void __launch_bounds__(kGridThreads, 1)
         }
         if (ahead.i < nmine) cur_next(ahead);
       }
+      if (thi < z1 && thi >= z0) emit_rows(thi + 1, acc_a);  // plane z1 does not exist: row z1-1 is done
     }
   }
 
@@ -359,9 +399,9 @@ __global__ void __launch_bounds__(kGridThreads, 1)
 
 // Dynamic shared memory of k1_grid with a ring of ns stages.
 template <int K, int P, bool GLOBAL>
-int k1_grid_smem(int ns) {
+int k1_grid_smem(int ns, bool var) {
   using S = FastSmem<K, P, 1, GLOBAL>;
-  const int main = ns * kGridStageBytes + ns * 8 + ns * 4;
+  const int main = ns * (var ? kGridStageBytesVar : kGridStageBytes) + ns * 8 + ns * 4;
   const int epi = (int)sizeof(double) *
                   (32 * 8 * (K / kGridW) + 3 * S::CS + bsolve_ws_doubles(P, kGridThreads) + K);
   return (main > epi ? main : epi) + 1024;  // + alignment slack

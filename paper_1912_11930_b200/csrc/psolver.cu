@@ -189,8 +189,8 @@ struct Part {
   // are separate launches over the ghost-extended P seen as a tensor
   GridStencil gst;
   GridArgs ga_in{}, ga_bd{};
-  struct alignas(64) TensorMap {
-    unsigned char bytes[128];
+  struct alignas(64) TensorMap {  // GridMaps of kernels_grid.cuh: p (v5, v1 unused)
+    unsigned char bytes[3 * 128];
   } tmap[2];
   Ctrl* ctrl() { return reinterpret_cast<Ctrl*>(ctrl_buf.ptr); }
 };
@@ -332,7 +332,7 @@ struct bkg_psolver {
     grid_stencil_rows(ctx, pt.nloc, pt.A.rowptr.ptr, pt.A.cols.ptr, pt.A.vals.ptr, pt.r0, n,
                       pt.gst);
     const GridStencil& st = pt.gst;
-    if (!st.ok) return false;
+    if (!st.ok) return false;  // (variable coefficients: whole matrices only)
     const int64_t plane = (int64_t)st.nx * st.ny;
     const bool lower = st.zs > 0, upper = st.zs + st.nz < st.nzg;
     if (pt.lo != pt.r0 - (lower ? plane : 0) || pt.hi != pt.r1 + (upper ? plane : 0)) return false;
@@ -343,7 +343,7 @@ struct bkg_psolver {
     if (ns < 2) return false;
     pt.k1_kind = 4;
     pt.k1 = ft.k1_grid[st.full27 ? 1 : 0];  // + 2: paced (interior launch, chosen per launch)
-    pt.smem_k1 = ft.grid_smem(ns);
+    pt.smem_k1 = ft.grid_smem(ns, false);
     for (int v = 0; v < 4; ++v) allow_smem(ft.k1_grid[v], pt.smem_k1);
     const int zoff = lower ? 1 : 0;
     const int zb = lower ? 1 : 0, ze = upper ? st.nz - 1 : st.nz;
@@ -351,18 +351,18 @@ struct bkg_psolver {
     const int reserve = use_nccl && nranks > 1 ? (hs ? std::atoi(hs) : 4) : 0;
     pt.nin = pt.nbd = 0;
     pt.g1i = pt.g1b = 1;
+    const int nzt = (int)((pt.hi - pt.lo) / plane);
     if (ze > zb) {
-      grid_plan(st, k, std::max(1, ctx->sm_count - reserve), ns, zb, ze, zoff, &pt.ga_in,
+      grid_plan(st, k, std::max(1, ctx->sm_count - reserve), ns, zb, ze, zoff, nzt, &pt.ga_in,
                 &pt.g1i);
       pt.nin = pt.ga_in.nitems;
     }
     if (lower || upper) {
       const bool lo_end = lower, up_end = upper && !(lower && st.nz == 1);
-      grid_plan_ends(st, k, ctx->sm_count, ns, lo_end, up_end, zoff, &pt.ga_bd, &pt.g1b);
+      grid_plan_ends(st, k, ctx->sm_count, ns, lo_end, up_end, zoff, nzt, &pt.ga_bd, &pt.g1b);
       pt.nbd = pt.ga_bd.nitems;
     }
     pt.g1 = std::max(pt.g1i, pt.g1b);
-    const int nzt = (int)((pt.hi - pt.lo) / plane);
     for (int i = 0; i < (defer ? 2 : 1); ++i)
       grid_tensor_map(pt.Pext[i].ptr, k, st.nx, st.ny, nzt, pt.tmap[i].bytes);
     return true;

@@ -1,5 +1,5 @@
-"""k1_grid (kernels_grid.cuh): K1 for matrices that are exactly a 3-D 7- or
-27-point constant-coefficient grid stencil, applied from TMA-tiled operand
+"""k1_grid (kernels_grid.cuh): K1 for matrices that are exactly a 2-D 5/9-point
+or 3-D 7/27-point constant-coefficient grid stencil, applied from TMA-tiled operand
 planes (cp.async.bulk.tensor.4d, zero-filled halos) instead of the CSR stream.
 The structure is verified entry by entry on device (grid.cu); anything else
 keeps the CSR kernels.  BKG_K1_GRID=1 forces it here at every size: first K1
@@ -55,7 +55,8 @@ def _first_step(port, csr, n, k, p, glob, expect_grid):
 @pytest.mark.parametrize("k,p,glob", SHAPES)
 @pytest.mark.parametrize("kind,dims", [(3, (33, 17, 9)), (4, (11, 19, 13)), (3, (16, 16, 16)),
                                        (4, (32, 16, 5)), (3, (6, 5, 4)), (4, (5, 4, 6)),
-                                       (3, (47, 35, 3))])
+                                       (3, (47, 35, 3)), (0, (40, 30, 1)), (0, (77, 31, 1)),
+                                       (0, (16, 16, 1))])
 def test_grid_first_step(port, grid_on, k, p, glob, kind, dims):
     a = bk.stencil(kind, *dims, seed=11)
     _first_step(port, _csr(a), a.n(), k, p, glob, True)
@@ -78,19 +79,25 @@ def test_grid_first_step_ring_depths(port, grid_on, monkeypatch, ns):
     _first_step(port, _csr(a), a.n(), 64, 16, False, True)
 
 
-def test_grid_rejects_everything_else(port, grid_on):
-    """2-D grids, variable coefficients, irregular patterns and a stencil with
-    one entry changed or removed keep the CSR kernels (and stay correct)."""
-    for kind, dims in [(0, (40, 30, 1)), (1, (32, 32, 1)), (2, (32, 24, 1))]:
+def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
+    """Variable coefficients on a 5 / 7-point star run k1_grid from the DIA
+    tiles (2-D heterogeneous Poisson, the C3 lognormal field, a 7-point stencil
+    with one value changed or one entry pair removed); an odd nx (TMA stride),
+    BKG_GRID_VAR=0 and irregular patterns keep the CSR kernels.  All correct."""
+    for kind, dims in [(1, (32, 32, 1)), (2, (32, 24, 1)), (2, (70, 33, 1))]:
         a = bk.stencil(kind, *dims, seed=11)
-        _first_step(port, _csr(a), a.n(), 16, 4, False, False)
+        for k, p, glob in [(16, 4, False), (64, 1, False), (64, 4, True), (32, 8, False)]:
+            _first_step(port, _csr(a), a.n(), k, p, glob, True)
+    a = bk.stencil(1, 33, 20, 1, seed=11)  # odd nx
+    _first_step(port, _csr(a), a.n(), 16, 4, False, False)
     _first_step(port, irregular(1001, seed=5), 1001, 16, 4, False, False)
     a = bk.stencil(3, 12, 11, 10, seed=11)
     rp, ci, v = (np.array(x) for x in _csr(a))
     n = a.n()
     v2 = v.copy()
     v2[int(rp[n // 3]) + 1] *= 1.0 + 2.0 ** -50  # one coefficient off by a few ulp
-    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
+    _first_step(port, (rp, ci, v2), n, 16, 4, False, True)
+    _first_step(port, (rp, ci, v2), n, 64, 16, False, True)
     # remove one off-diagonal entry and its symmetric counterpart
     row = n // 2 + 3
     e = int(rp[row])
@@ -104,10 +111,37 @@ def test_grid_rejects_everything_else(port, grid_on):
     cnt[row] -= 1
     cnt[col] -= 1
     rp3 = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64)
-    _first_step(port, (rp3, ci[keep], v[keep]), n, 16, 4, False, False)
-    # a small 27-point grid is accepted
+    _first_step(port, (rp3, ci[keep], v[keep]), n, 16, 4, False, True)
+    monkeypatch.setenv("BKG_GRID_VAR", "0")
+    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
+    monkeypatch.delenv("BKG_GRID_VAR")
+    # a small 27-point grid is accepted (constant path)
     a4 = bk.stencil(4, 9, 8, 7, seed=11)
     _first_step(port, _csr(a4), a4.n(), 16, 4, False, True)
+
+
+@pytest.mark.parametrize("k,p,glob", [(64, 1, False), (64, 4, True), (16, 16, False)])
+def test_grid_variable_solve_agrees_with_csr_kernels(grid_on, monkeypatch, k, p, glob):
+    """C3's lognormal diffusion at reduced size: whole fast solves with the
+    variable-coefficient k1_grid and with k1_wide.  The field is reorder-chaotic
+    (DESIGN.md §2 floor), so the bars are X 1e-8 and iterations within 5%."""
+    a = bk.stencil(2, 96, 80, 1, seed=11)
+    n = a.n()
+    b = bk.random_block_rhs(n, k, 7)
+    cfg = bk.SubalgebraConfig(k, p, "global" if glob else "hybrid")
+    opts = bk.SolveOptions(tol=1e-10, max_iter=20000)
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("BKG_K1_GRID", v)
+        ctx = bk.Context(0, "fast")
+        res = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), cfg, opts, ctx=ctx)
+        assert ctx.last_k1() == ("k1_grid" if v == "1" else "k1_wide")
+        assert res.report.converged
+        out[v] = (res.x, res.report.iterations)
+        ctx.close()
+    xr = np.linalg.norm(out["1"][0] - out["0"][0], axis=0) / np.linalg.norm(out["0"][0], axis=0)
+    assert np.max(xr) <= 1e-8, xr
+    assert abs(out["1"][1] - out["0"][1]) <= max(1, int(0.05 * out["0"][1]))
 
 
 @pytest.mark.parametrize("kind,k,p,glob", [(3, 32, 8, False), (3, 64, 16, False), (3, 64, 4, True),
