@@ -169,8 +169,10 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
   if (hbad) {
     // not one value per offset: variable coefficients on a 5 / 7-point star?
     // (whole matrices; TMA strides need an even nx)
+    // Opt-in (BKG_GRID_VAR=1): on C3 (2-D, one plane per item) it is only 3%
+    // faster than k1_wide.
     const char* ev = std::getenv("BKG_GRID_VAR");
-    if (r0 != 0 || nglobal != n || (nx & 1) || (ev && ev[0] == '0')) return;
+    if (r0 != 0 || nglobal != n || (nx & 1) || !ev || ev[0] != '1') return;
     st.dia.alloc((size_t)7 * n);
     BKG_CUDA_CHECK(cudaMemsetAsync(st.dia.ptr, 0, st.dia.bytes(), c->stream));
     BKG_CUDA_CHECK(cudaMemsetAsync(bad.ptr, 0, sizeof(int), c->stream));

@@ -82,8 +82,10 @@ def test_grid_first_step_ring_depths(port, grid_on, monkeypatch, ns):
 def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
     """Variable coefficients on a 5 / 7-point star run k1_grid from the DIA
     tiles (2-D heterogeneous Poisson, the C3 lognormal field, a 7-point stencil
-    with one value changed or one entry pair removed); an odd nx (TMA stride),
-    BKG_GRID_VAR=0 and irregular patterns keep the CSR kernels.  All correct."""
+    with one value changed or one entry pair removed; opt-in BKG_GRID_VAR=1); an
+    odd nx (TMA stride), the default and irregular patterns keep the CSR kernels.
+    All correct."""
+    monkeypatch.setenv("BKG_GRID_VAR", "1")
     for kind, dims in [(1, (32, 32, 1)), (2, (32, 24, 1)), (2, (70, 33, 1))]:
         a = bk.stencil(kind, *dims, seed=11)
         for k, p, glob in [(16, 4, False), (64, 1, False), (64, 4, True), (32, 8, False)]:
@@ -112,9 +114,8 @@ def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
     cnt[col] -= 1
     rp3 = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64)
     _first_step(port, (rp3, ci[keep], v[keep]), n, 16, 4, False, True)
-    monkeypatch.setenv("BKG_GRID_VAR", "0")
-    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
     monkeypatch.delenv("BKG_GRID_VAR")
+    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
     # a small 27-point grid is accepted (constant path)
     a4 = bk.stencil(4, 9, 8, 7, seed=11)
     _first_step(port, _csr(a4), a4.n(), 16, 4, False, True)
@@ -125,6 +126,7 @@ def test_grid_variable_solve_agrees_with_csr_kernels(grid_on, monkeypatch, k, p,
     """C3's lognormal diffusion at reduced size: whole fast solves with the
     variable-coefficient k1_grid and with k1_wide.  The field is reorder-chaotic
     (DESIGN.md §2 floor), so the bars are X 1e-8 and iterations within 5%."""
+    monkeypatch.setenv("BKG_GRID_VAR", "1")
     a = bk.stencil(2, 96, 80, 1, seed=11)
     n = a.n()
     b = bk.random_block_rhs(n, k, 7)
