@@ -700,7 +700,8 @@ int bkg::grid_ring_depth(const FastTable& ft, int K, int per_cta) {
 }
 
 bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g,
-                   int* ctas, int* smem) {
+                   int* ctas, int* smem, bool* two_d) {
+  *two_d = false;
   if (!ft.k1_grid[0] || A->n == 0) return false;
   const char* env = std::getenv("BKG_K1_GRID");
   if (env && env[0] == '0') return false;
@@ -714,6 +715,18 @@ bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, 
   int optin = 0;
   BKG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const int per_cta = std::min(optin, 227 * 1024);
+  const char* e2 = std::getenv("BKG_GRID2");
+  if (st.nz == 1 && !(e2 && e2[0] == '0') && !(st.var && st.full27)) {
+    // 2-D: lines of 128 points marching in y (kernels_grid2.cuh), 2 CTAs per SM
+    const char* en = std::getenv("BKG_GRID_NS");
+    int ns = en ? std::max(2, std::atoi(en)) : 3;  // B200 sweep: 3 <= 4..6 on every 2-D case
+    while (ns > 2 && ft.grid2_smem(ns, st.var) > per_cta / 2 - 1024) --ns;
+    grid2_plan(st, K, c->sm_count, ns, g, ctas);
+    *smem = ft.grid2_smem(ns, st.var);
+    for (int v = 0; v < 3; ++v) allow_smem(ft.k1_grid2[v], *smem);
+    *two_d = true;
+    return true;
+  }
   const int ns = grid_ring_depth(ft, st.var ? -K : K, per_cta);
   if (ns < 2) return false;
   grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, st.nz, g, ctas);
@@ -874,6 +887,7 @@ struct bkg_solver {
   int k1_kind = 0;   // 0 k1_wide, 1 k1_line, 2 k1_stage, 4 k1_grid
   // k1_grid (kernels_grid.cuh): plan and one TMA tensor map per P buffer
   GridArgs grid_args{};
+  bool grid_2d = false;  // k1_grid2 (2-D grids, kernels_grid2.cuh)
   struct alignas(64) TensorMap {
     unsigned char bytes[128];
   };
@@ -1030,13 +1044,16 @@ struct bkg_solver {
     k1_kind = 0;
     k1_threads = kThreads;
     int smem = 0;
-    if (use_grid(ctx, A, ft, k, &grid_args, &g1, &smem)) {
+    if (use_grid(ctx, A, ft, k, &grid_args, &g1, &smem, &grid_2d)) {
       k1_kind = 4;
-      ft.k1 = A->gridst.var
-                  ? ft.k1_grid[4 + (grid_args.sync_every > 0 ? 1 : 0)]
-                  : ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
+      if (grid_2d)
+        ft.k1 = ft.k1_grid2[A->gridst.var ? 2 : (A->gridst.full27 ? 1 : 0)];
+      else
+        ft.k1 = A->gridst.var
+                    ? ft.k1_grid[4 + (grid_args.sync_every > 0 ? 1 : 0)]
+                    : ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
       ft.smem_k1 = smem;
-      k1_threads = kGridThreads;
+      k1_threads = grid_2d ? kG2Threads : kGridThreads;
       grid_maps.clear();
       return;
     }
@@ -1084,10 +1101,18 @@ struct bkg_solver {
         const GridStencil& gs = A->gridst;
         grid_maps.emplace_back(a.P, GridMapSet{});
         tm = &grid_maps.back().second;
-        grid_tensor_map(a.P, k, gs.nx, gs.ny, gs.nz, tm->bytes);
-        if (gs.var) {
-          grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 5, tm->bytes + 128);
-          grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 1, tm->bytes + 256);
+        if (grid_2d) {
+          grid2_tensor_map(a.P, k, gs.nx, gs.ny, tm->bytes);
+          if (gs.var) {
+            grid2_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, 3, tm->bytes + 128);
+            grid2_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, 1, tm->bytes + 256);
+          }
+        } else {
+          grid_tensor_map(a.P, k, gs.nx, gs.ny, gs.nz, tm->bytes);
+          if (gs.var) {
+            grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 5, tm->bytes + 128);
+            grid_dia_tensor_map(gs.dia.ptr, gs.nx, gs.ny, gs.nz, 1, tm->bytes + 256);
+          }
         }
       }
       void* args[] = {&a, &grid_args, tm->bytes};

@@ -10,6 +10,7 @@
 #include "kernels_resident.cuh"
 #include "kernels_stage.cuh"
 #include "kernels_grid.cuh"
+#include "kernels_grid2.cuh"
 #include "kernels_tma.cuh"
 
 // K1 implementation: 1 = k1_wide (kernels_k1.cuh, 256-bit gathers), 0 = k1_tile.
@@ -96,6 +97,9 @@ struct FastTable {
   const void* k1_grid[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool grid_auto = false;  // the solver may pick it without BKG_K1_GRID=1
   int (*grid_smem)(int ns, bool var) = nullptr;
+  // 2-D grids (kernels_grid2.cuh): [0] 5-point, [1] 9-point, [2] 5-point variable
+  const void* k1_grid2[3] = {nullptr, nullptr, nullptr};
+  int (*grid2_smem)(int ns, bool var) = nullptr;
   // K2 / K3 with TMA-staged operand tiles (kernels_tma.cuh; M = I loop with
   // the deferred X update): k3_tma[0] skip, [1] flush
   const void* k2_tma = nullptr;
@@ -148,6 +152,10 @@ void fill_table(FastTable* t) {
       t->k1_grid[3] = (const void*)&k1_grid<K, P, G, true, true>;
       t->k1_grid[4] = (const void*)&k1_grid<K, P, G, false, false, true>;
       t->k1_grid[5] = (const void*)&k1_grid<K, P, G, false, true, true>;
+      t->k1_grid2[0] = (const void*)&k1_grid2<K, P, G, false, false>;
+      t->k1_grid2[1] = (const void*)&k1_grid2<K, P, G, true, false>;
+      t->k1_grid2[2] = (const void*)&k1_grid2<K, P, G, false, true>;
+      t->grid2_smem = &k1_grid2_smem<K, P, G>;
       t->grid_smem = &k1_grid_smem<K, P, G>;
       // B200: C5 K1 6.93 -> 3.07 ms, C2 0.354 -> 0.207, C4 1.87 -> 0.44
       t->grid_auto = true;

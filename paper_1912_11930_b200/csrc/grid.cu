@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "host.cuh"
 #include "kernels_grid.cuh"
+#include "kernels_grid2.cuh"
 
 namespace bkg {
 
@@ -169,10 +170,11 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
   if (hbad) {
     // not one value per offset: variable coefficients on a 5 / 7-point star?
     // (whole matrices; TMA strides need an even nx)
-    // Opt-in (BKG_GRID_VAR=1): on C3 (2-D, one plane per item) it is only 3%
-    // faster than k1_wide.
+    // BKG_GRID_VAR=0/1 forces it off/on; default: 2-D grids only (k1_grid2:
+    // C3 K1 0.313 -> 0.215 ms; the 3-D variant is unmeasured at scale).
     const char* ev = std::getenv("BKG_GRID_VAR");
-    if (r0 != 0 || nglobal != n || (nx & 1) || !ev || ev[0] != '1') return;
+    const bool want = ev ? ev[0] == '1' : nzg == 1;
+    if (r0 != 0 || nglobal != n || (nx & 1) || !want) return;
     st.dia.alloc((size_t)7 * n);
     BKG_CUDA_CHECK(cudaMemsetAsync(st.dia.ptr, 0, st.dia.bytes(), c->stream));
     BKG_CUDA_CHECK(cudaMemsetAsync(bad.ptr, 0, sizeof(int), c->stream));
@@ -263,6 +265,49 @@ void grid_plan(const GridStencil& st, int K, int sm_count, int ns, int zbeg, int
   g->sync_lead = el ? std::max(0, std::atoi(el)) : 1;
 }
 
+// 2-D grids (k1_grid2, kernels_grid2.cuh): items = (y-chunk, 128-point x tile,
+// slice) for a persistent grid of 2 CTAs per SM; y-chunk by the same score.
+void grid2_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, int* ctas) {
+  const int nsl = K / kGridW;
+  std::memset(g, 0, sizeof(*g));
+  g->nx = st.nx;
+  g->ny = st.ny;
+  g->nz = 1;
+  g->tx = (st.nx + kG2BX - 1) / kG2BX;
+  g->ty = 1;
+  g->ns = ns;
+  g->zbeg = 0;
+  g->zend = st.ny;
+  g->zoff = 0;
+  g->tmin = 0;
+  g->tmax = st.ny - 1;
+  std::memcpy(g->c, st.c, sizeof(g->c));
+  const int64_t T = (int64_t)g->tx * nsl;
+  const int64_t G = std::max<int64_t>(nsl, (int64_t)(2 * sm_count / nsl) * nsl);
+  double best = -1.0;
+  int best_chunk = st.ny;
+  for (int nyc = 1; nyc <= std::max(1, st.ny / 8); ++nyc) {
+    const int chunk = (st.ny + nyc - 1) / nyc;
+    const int real = (st.ny + chunk - 1) / chunk;
+    const int64_t items = T * real;
+    const int64_t grid = std::min(G, items);
+    const int64_t rounds = (items + grid - 1) / grid;
+    const double util = (double)items / (double)(rounds * grid) * ((double)grid / (double)G);
+    const double score = util / (1.0 + 2.0 / chunk);
+    if (score > best * 1.0001) {
+      best = score;
+      best_chunk = chunk;
+    }
+  }
+  const char* ez = std::getenv("BKG_GRID_ZCHUNK");
+  if (ez && std::atoi(ez) > 0) best_chunk = std::min(st.ny, std::atoi(ez));
+  g->zchunk = best_chunk;
+  g->zstride = best_chunk;
+  g->nzc = (st.ny + best_chunk - 1) / best_chunk;
+  g->nitems = T * g->nzc;
+  *ctas = (int)std::min(G, g->nitems);
+}
+
 // The two single-plane items per (tile, slice) at the ends of a z-slab part:
 // planes 0 and nz - 1 (the rows that read the neighbours' ghost planes).
 void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool lower, bool upper,
@@ -334,6 +379,36 @@ void grid_dia_tensor_map(const double* V, int nx, int ny, int nz, int slots, voi
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
               "cuTensorMapEncodeTiled (DIA) failed (" + std::to_string((int)rc) + ")");
+}
+
+// k1_grid2: a row-major n x K block vector of a 2-D grid as (column, x, y), box =
+// 16 columns x one 128-point line tile with its two x neighbours; and its DIA
+// copy as (x, y, slot), boxes of `slots` slots.
+void grid2_tensor_map(const double* P, int K, int nx, int ny, void* out) {
+  EncodeFn encode = tensor_map_encoder();
+  const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)nx, (cuuint64_t)ny};
+  const cuuint64_t strides[2] = {(cuuint64_t)K * 8, (cuuint64_t)K * 8 * nx};
+  const cuuint32_t box[3] = {kGridW, kG2BX + 2, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             3, const_cast<double*>(P), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
+              "cuTensorMapEncodeTiled (2-D grid) failed (" + std::to_string((int)rc) + ")");
+}
+void grid2_dia_tensor_map(const double* V, int nx, int ny, int slots, void* out) {
+  EncodeFn encode = tensor_map_encoder();
+  const cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, 7};
+  const cuuint64_t strides[2] = {(cuuint64_t)8 * nx, (cuuint64_t)8 * nx * ny};
+  const cuuint32_t box[3] = {kG2BX, 1, (cuuint32_t)slots};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                             3, const_cast<double*>(V), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  BKG_REQUIRE(rc == CUDA_SUCCESS, BKG_CUDA,
+              "cuTensorMapEncodeTiled (2-D DIA) failed (" + std::to_string((int)rc) + ")");
 }
 
 void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out) {

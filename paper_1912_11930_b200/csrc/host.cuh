@@ -22,7 +22,7 @@ bool use_fast(const bkg_ctx* c, int k, int p, bool global, FastTable* t);
 bool use_stage(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, int* ns, int* smem);
 bool use_line(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft);
 bool use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, GridArgs* g, int* ctas,
-              int* smem);
+              int* smem, bool* two_d);
 // grid.cu: constant-coefficient grid stencil detection, k1_grid plan and tensor map
 const GridStencil& grid_stencil(bkg_ctx* c, const bkg_matrix* A);
 void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32_t* cols,
@@ -33,6 +33,10 @@ void grid_plan_ends(const GridStencil& st, int K, int sm_count, int ns, bool low
                     int zoff, int nzt, GridArgs* g, int* ctas);
 void grid_tensor_map(const double* P, int K, int nx, int ny, int nz, void* out);
 void grid_dia_tensor_map(const double* V, int nx, int ny, int nz, int slots, void* out);
+// 2-D grids (k1_grid2)
+void grid2_plan(const GridStencil& st, int K, int sm_count, int ns, GridArgs* g, int* ctas);
+void grid2_tensor_map(const double* P, int K, int nx, int ny, void* out);
+void grid2_dia_tensor_map(const double* V, int nx, int ny, int slots, void* out);
 int grid_ring_depth(const FastTable& ft, int K, int per_cta);
 // 2-D tensor map of a row-major n x K block vector, box = 16 columns x `rows` rows
 void tile_tensor_map(const double* P, int K, int64_t n, int rows, void* out);

@@ -32,7 +32,14 @@ class Gen:
     random_block_rhs = staticmethod(bk.random_block_rhs)
 
 
-def solve(name, numerics):
+# Exact mode's global-subalgebra Grams are p^2 serial chains over all n k / p
+# products (3.6 s per iteration on C4): that case runs the first 40 of its 200
+# iterations and is compared with the fixture's history prefix (the whole run
+# is 12 minutes, more than the rest of the GPU suite together).
+EXACT_PREFIX = {"c4_full_global4": 40}
+
+
+def solve(name, numerics, max_iter=None):
     case = BY_NAME[name]
     csr, b, x0 = build_inputs(case, Gen())
     g = golden_io.load(name)
@@ -41,7 +48,8 @@ def solve(name, numerics):
     ctx = bk.Context(0, numerics)
     res = bk.bcg_solve(a, b, bk.Preconditioner.identity(a.n()),
                        bk.SubalgebraConfig(case.k, case.p, case.mode),
-                       bk.SolveOptions(tol=case.tol, max_iter=case.max_iter, record_history=True),
+                       bk.SolveOptions(tol=case.tol, max_iter=max_iter or case.max_iter,
+                                       record_history=True),
                        ctx=ctx)
     res.k1 = ctx.last_k1()
     a.release_device()
@@ -51,6 +59,14 @@ def solve(name, numerics):
 
 @pytest.mark.parametrize("name", EXACT_OK)
 def test_full_exact_bit_identical(name):
+    if name in EXACT_PREFIX:
+        it = EXACT_PREFIX[name]
+        res, g = solve(name, "exact", max_iter=it)
+        assert res.report.iterations == it < g["meta"]["iterations"]
+        h = np.array(res.report.defect_history)
+        assert h.shape[0] == it + 1
+        assert h.tobytes() == g["history"][:it + 1].tobytes()
+        return
     res, g = solve(name, "exact")
     m = g["meta"]
     r = res.report

@@ -114,8 +114,13 @@ def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
     cnt[col] -= 1
     rp3 = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64)
     _first_step(port, (rp3, ci[keep], v[keep]), n, 16, 4, False, True)
-    monkeypatch.delenv("BKG_GRID_VAR")
+    monkeypatch.delenv("BKG_GRID_VAR")  # default: variable coefficients on 2-D grids only
     _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
+    a2 = bk.stencil(2, 32, 24, 1, seed=11)
+    _first_step(port, _csr(a2), a2.n(), 16, 4, False, True)
+    monkeypatch.setenv("BKG_GRID_VAR", "0")
+    _first_step(port, _csr(a2), a2.n(), 16, 4, False, False)
+    monkeypatch.delenv("BKG_GRID_VAR")
     # a small 27-point grid is accepted (constant path)
     a4 = bk.stencil(4, 9, 8, 7, seed=11)
     _first_step(port, _csr(a4), a4.n(), 16, 4, False, True)
@@ -197,3 +202,29 @@ def test_grid_and_wide_agree_on_large_system(monkeypatch, kind, dims, k, p):
                                                                                   axis=0)
     assert np.max(xr) <= 1e-9, xr
     assert out["grid"][0].tobytes() == out["grid2"][0].tobytes()
+
+
+@pytest.mark.parametrize("k,p", [(16, 4), (64, 16), (32, 8)])
+def test_grid2_solve_agrees_with_csr_kernels(monkeypatch, k, p):
+    """2-D constant 5-point Poisson through k1_grid2 (128-point line tiles
+    marching in y, kernels_grid2.cuh) and through the CSR kernels: fixed
+    iteration count, X 1e-8, history within 5e-9 (the reference's own
+    reordering floor on 2-D Poisson is 6.6e-10)."""
+    a = bk.stencil(0, 300, 257, 1, seed=11)
+    n = a.n()
+    b = bk.normal_block_rhs(n, k, 7)
+    cfg = bk.SubalgebraConfig(k, p, "hybrid")
+    opts = bk.SolveOptions(tol=1e-300, max_iter=60, record_history=True)
+    out = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("BKG_K1_GRID", v)
+        monkeypatch.setenv("BKG_K1_LINE", "0")
+        monkeypatch.setenv("BKG_K1_STAGE", "0")
+        ctx = bk.Context(0, "fast")
+        res = bk.bcg_solve(a, b, bk.Preconditioner.identity(n), cfg, opts, ctx=ctx)
+        assert ctx.last_k1() == ("k1_grid" if v == "1" else "k1_wide")
+        out[v] = (res.x, np.array(res.report.defect_history))
+        ctx.close()
+    assert _drift(out["1"][1], out["0"][1]) <= 5e-9
+    xr = np.linalg.norm(out["1"][0] - out["0"][0], axis=0) / np.linalg.norm(out["0"][0], axis=0)
+    assert np.max(xr) <= 1e-8, xr
