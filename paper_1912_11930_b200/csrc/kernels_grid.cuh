@@ -1,5 +1,5 @@
-// kernels_grid.cuh — K1 for constant-coefficient grid stencils, the operand
-// planes tiled through shared memory by TMA tensor copies: Q = A P
+// kernels_grid.cuh — K1 for grid stencils (3-D; 2-D grids: kernels_grid2.cuh), the
+// operand planes tiled through shared memory by TMA tensor copies: Q = A P
 // (kernels.hpp:129-157), alpha = <<P, Q>> (kernels.hpp:59-88), last CTA:
 // lambda = alpha^-1 rho_prev (kernels.hpp:231-240).
 //
@@ -11,7 +11,10 @@
 // 16 x 16 tile of one z-plane plus its one-point halo, 16 columns wide, is ONE
 // cp.async.bulk.tensor.4d copy (box 16 x 18 x 18 x 1, SWIZZLE_128B; the halo
 // outside the grid is zero-filled by the TMA unit, which is exactly the
-// truncated row).  No CSR index or value is read in the loop.
+// truncated row).  No CSR index or value is read in the loop.  (VAR: the
+// values differ from row to row on a 5 / 7-point star; the stage then also
+// receives the tile's coefficients from a DIA copy, three more tensor copies.)
+// Planes outside the tensor are neither copied nor computed.
 //
 // Work item = (z-chunk, tile, 16-column slice); CTA j of a persistent grid
 // takes items j, j + grid, ... (slice fastest, then x tiles: concurrently
@@ -36,6 +39,10 @@
 // read from shared memory 5 / 9 times instead of 7 / 27.  A row's products
 // are summed plane by plane (dz = -1, 0, +1), a different order from the CSR
 // kernels: fast-mode parity bars only.
+//
+// Long launches pace their persistent CTAs against a grid-wide counter (PACE,
+// GridArgs::sync_every) so that neighbouring tiles stay within a few planes of
+// each other and find their shared halo rows in L2.
 #pragma once
 
 #include <cuda.h>

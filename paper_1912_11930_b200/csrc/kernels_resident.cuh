@@ -60,10 +60,16 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
 }
 
 // Per-CTA sum of per-thread accumulators over the threads sharing
-// pos = tid % TPR, fixed order: red[pos * NACC + e].
+// pos = tid % TPR, fixed order: red[pos * NACC + e].  Every warp deposits its
+// (shuffle-reduced) partials side by side and E threads then add the 8 warps'
+// values in warp order -- the same sum as eight serial rounds of one warp
+// each, in two barriers instead of nine (the serial form was 13% of a C1
+// iteration).  part: (kThreads / 32) * TPR * NACC doubles of shared memory.
 template <int TPR, int NACC>
-__device__ __forceinline__ void cta_reduce(double (&acc)[NACC], double* red) {
+__device__ __forceinline__ void cta_reduce(double (&acc)[NACC], double* red, double* part) {
   constexpr int E = TPR * NACC;
+  constexpr int NW = kThreads / 32;
+  static_assert(TPR <= 32, "every warp holds every position");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pos = tid % TPR;
   if constexpr (TPR < 32) {
@@ -73,16 +79,120 @@ __device__ __forceinline__ void cta_reduce(double (&acc)[NACC], double* red) {
       for (int e = 0; e < NACC; ++e) acc[e] += __shfl_xor_sync(kFull, acc[e], off);
   }
   const bool rep = (TPR >= 32) || (lane < TPR);
-  for (int i = tid; i < E; i += kThreads) red[i] = 0.0;
-  __syncthreads();
-#pragma unroll 1
-  for (int w = 0; w < kThreads / 32; ++w) {
-    if (warp == w && rep) {
+  if (rep) {
 #pragma unroll
-      for (int e = 0; e < NACC; ++e) red[pos * NACC + e] += acc[e];
-    }
-    __syncthreads();
+    for (int e = 0; e < NACC; ++e) part[(size_t)warp * E + pos * NACC + e] = acc[e];
   }
+  __syncthreads();
+  for (int i = tid; i < E; i += kThreads) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += part[(size_t)w * E + i];
+    red[i] = s;
+  }
+  __syncthreads();
+}
+
+// gamma_b^-1 delta_b for every p x p block with one warp per block, in the
+// operation order of detail::solve_block (kernels.hpp:171-224), as cta_bsolve
+// (bsolve.cuh) -- same max-norm / 1e-14 breakdown test, same "first strictly
+// larger" pivot rule, unfused multiply / subtract per element in the same
+// sequence -- but without a CTA barrier per elimination step: lane c < P owns
+// column c of the block, lane P + c column c of the right-hand side, both in
+// registers; multipliers and pivots travel by shuffles.  cta_bsolve's 4
+// barriers and single-thread pivot search per column made the two solves 47%
+// of a C1 iteration.  Returns the smallest failing block or -1 to every thread.
+// gamma, delta, out: shared memory; bad_s: one int of shared memory.
+template <int P>
+__device__ int warp_bsolve(int nblk, const double* gamma, const double* delta, double* out,
+                           int* bad_s) {
+  static_assert(P >= 1 && P <= 16, "one warp holds [A | B]");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) *bad_s = INT_MAX;
+  __syncthreads();
+  for (int blk = warp; blk < nblk; blk += kThreads / 32) {
+    const bool isa = lane < P, isb = lane >= P && lane < 2 * P;
+    const int cidx = isa ? lane : lane - P;
+    const double* src = (isa ? gamma : delta) + (size_t)blk * P * P;
+    double col[P], inv[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) col[r] = (isa || isb) ? src[r * P + cidx] : 0.0;
+    // max-norm of the block (kernels.hpp:177-179)
+    double m = 0.0;
+    if (isa) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const double v = fabs(col[r]);
+        m = (m < v) ? v : m;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v = __shfl_xor_sync(kFull, m, o);
+      m = (m < v) ? v : m;
+    }
+    const double tiny = __dmul_rn(1e-14, m);
+    bool broke = false;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      // pivot search in column k by its owner, reference order (kernels.hpp:182-195)
+      int prow = k;
+      double pv = fabs(col[k]);
+#pragma unroll
+      for (int r = k + 1; r < P; ++r) {
+        const double cand = fabs(col[r]);
+        if (cand > pv) {
+          pv = cand;
+          prow = r;
+        }
+      }
+      prow = __shfl_sync(kFull, prow, k);
+      pv = __shfl_sync(kFull, pv, k);
+      if (pv < tiny || m == 0.0) {
+        broke = true;
+        break;
+      }
+      // row swap (every column, right-hand sides included: the permuted delta)
+#pragma unroll
+      for (int r = k + 1; r < P; ++r)
+        if (r == prow) {
+          const double t = col[k];
+          col[k] = col[r];
+          col[r] = t;
+        }
+      inv[k] = __ddiv_rn(1.0, __shfl_sync(kFull, col[k], k));
+      // elimination: f = lu[r][k] * inv; lu[r][c] -= f * lu[k][c] for c > k and
+      // every right-hand side (the forward substitution, same order in k)
+#pragma unroll
+      for (int r = k + 1; r < P; ++r) {
+        const double f = __dmul_rn(__shfl_sync(kFull, col[r], k), inv[k]);
+        if (lane > k) col[r] = __dsub_rn(col[r], __dmul_rn(f, col[k]));
+      }
+    }
+    if (broke) {
+      if (lane == 0) atomicMin(bad_s, blk);
+      continue;
+    }
+    // backward substitution (kernels.hpp:216-223): right-hand-side lanes
+#pragma unroll
+    for (int r = P - 1; r >= 0; --r) {
+      double accv = col[r];
+#pragma unroll
+      for (int j = r + 1; j < P; ++j) {
+        const double u = __shfl_sync(kFull, col[r], j);  // lu[r][j], column j's lane
+        if (isb) accv = __dsub_rn(accv, __dmul_rn(u, col[j]));
+      }
+      if (isb) col[r] = __dmul_rn(accv, inv[r]);
+    }
+    if (isb) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) out[(size_t)blk * P * P + r * P + cidx] = col[r];
+    }
+  }
+  __syncthreads();
+  const int bad = *bad_s;
+  __syncthreads();
+  return bad == INT_MAX ? -1 : bad;
 }
 
 // tot[e] = sum over all CTAs c (ascending) of pbuf[c * EB + e], computed by
@@ -144,7 +254,8 @@ struct ResidentSmem {
   static constexpr int EB2 = E + K;           // [rho | ||R_s||^2]
   static constexpr int RED = EB1 > kThreads ? EB1 : kThreads;
   static int bytes() {
-    return (int)sizeof(double) * (2 * RED + 5 * CS + K + bsolve_ws_doubles(P, kThreads));
+    // + the per-warp partials of cta_reduce and warp_bsolve's flag
+    return (int)sizeof(double) * (2 * RED + 5 * CS + K + (kThreads / 32) * EB1 + 2);
   }
 };
 
@@ -166,7 +277,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
   double* lam = rho + CS;
   double* beta = lam + CS;
   double* norms = beta + CS;  // K
-  double* ws = norms + K;
+  double* part = norms + K;  // (kThreads / 32) * EB1
+  int* bad_s = reinterpret_cast<int*>(part + (kThreads / 32) * S::EB1);
 
   const int tid = threadIdx.x, pos = tid % L::TPR, slot = tid / L::TPR, lane = tid & 31;
   const int col0 = pos * CPT;
@@ -264,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
     }
     tick(0);  // SpMM + alpha
     // acc layout per pos: [alpha NG | rho_prev' NG] -> pbuf1 as two E-blocks
-    cta_reduce<L::TPR, 2 * NG>(acc, red);
+    cta_reduce<L::TPR, 2 * NG>(acc, red, part);
     {
       double* mine = ra.pbuf1 + (size_t)blockIdx.x * S::EB1;
       for (int i = tid; i < S::EB1; i += kThreads) {
@@ -280,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
     gather_gram<K, P, CPT, GLOBAL, NG>(tot, 0, alpha);
     if (have_rp) gather_gram<K, P, CPT, GLOBAL, NG>(tot + E, 0, rhop);
     __syncthreads();
-    int bad = cta_bsolve<P>(S::NB, P, alpha, rhop, lam, ws);  // lambda (kernels.hpp:231-240)
+    int bad = warp_bsolve<P>(S::NB, alpha, rhop, lam, bad_s);  // lambda (kernels.hpp:231-240)
     tick(4);  // lambda solve
     if (bad >= 0) {  // singular alpha: X, R untouched (solver.hpp:192-195)
       if (cta0) record_breakdown(ctrl, bad, 1);
@@ -317,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
       for (int j = 0; j < CPT; ++j) acc2[NG + j] = fma(r[u][j], r[u][j], acc2[NG + j]);
     }
     tick(5);  // R update + rho
-    cta_reduce<L::TPR, NG + CPT>(acc2, red);
+    cta_reduce<L::TPR, NG + CPT>(acc2, red, part);
     {
       double* mine = ra.pbuf2 + (size_t)blockIdx.x * S::EB2;
       for (int i = tid; i < E; i += kThreads)
@@ -333,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
     gather_gram<K, P, CPT, GLOBAL, NG>(tot, 0, rho);
     for (int c = tid; c < K; c += kThreads) norms[c] = sqrt(tot[E + c]);
     __syncthreads();
-    bad = cta_bsolve<P>(S::NB, P, rhop, rho, beta, ws);  // beta = rho_prev^-1 rho
+    bad = warp_bsolve<P>(S::NB, rhop, rho, beta, bad_s);  // beta = rho_prev^-1 rho
     tick(9);  // beta solve
     // X += P lambda precedes the beta solve in the reference (solver.hpp:171-175)
 #pragma unroll
@@ -422,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_resident(ResidentArgs ra) {
       acc[e] = 0.0;
       acc[NG + e] = accp[e];
     }
-    cta_reduce<L::TPR, 2 * NG>(acc, red);
+    cta_reduce<L::TPR, 2 * NG>(acc, red, part);
     double* mine = ra.pbuf1 + (size_t)blockIdx.x * S::EB1;
     for (int i = tid; i < S::EB1; i += kThreads) {
       const int half = i / E, e = i % E;
