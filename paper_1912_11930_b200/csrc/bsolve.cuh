@@ -180,6 +180,130 @@ __device__ int cta_bsolve(int nblk, int p_rt, const double* gamma, const double*
   return bad == INT_MAX ? -1 : bad;
 }
 
+// gamma_b^-1 delta_b for every p x p block with one warp per block, in the
+// operation order of detail::solve_block (kernels.hpp:171-224), as cta_bsolve
+// (bsolve.cuh) -- same max-norm / 1e-14 breakdown test, same "first strictly
+// larger" pivot rule, unfused multiply / subtract per element in the same
+// sequence -- but without a CTA barrier per elimination step: lane c < P owns
+// column c of the block, lane P + c column c of the right-hand side, both in
+// registers; multipliers and pivots travel by shuffles.  cta_bsolve's 4
+// barriers and single-thread pivot search per column made the two solves 47%
+// of a C1 iteration.  Returns the smallest failing block or -1 to every thread.
+// gamma, delta, out: shared or global memory; bad_s: one int of shared memory.
+// Every thread of the CTA must call it (CTA barriers around the flag).
+template <int P>
+__device__ int warp_bsolve(int nblk, const double* gamma, const double* delta, double* out,
+                           int* bad_s) {
+  static_assert(P >= 1 && P <= 16, "one warp holds [A | B]");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) *bad_s = INT_MAX;
+  __syncthreads();
+  for (int blk = warp; blk < nblk; blk += (int)(blockDim.x >> 5)) {
+    const bool isa = lane < P, isb = lane >= P && lane < 2 * P;
+    const int cidx = isa ? lane : lane - P;
+    const double* src = (isa ? gamma : delta) + (size_t)blk * P * P;
+    double col[P], inv[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) col[r] = (isa || isb) ? src[r * P + cidx] : 0.0;
+    // max-norm of the block (kernels.hpp:177-179)
+    double m = 0.0;
+    if (isa) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const double v = fabs(col[r]);
+        m = (m < v) ? v : m;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = (m < v) ? v : m;
+    }
+    const double tiny = __dmul_rn(1e-14, m);
+    bool broke = false;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      // pivot search in column k by its owner, reference order (kernels.hpp:182-195)
+      int prow = k;
+      double pv = fabs(col[k]);
+#pragma unroll
+      for (int r = k + 1; r < P; ++r) {
+        const double cand = fabs(col[r]);
+        if (cand > pv) {
+          pv = cand;
+          prow = r;
+        }
+      }
+      prow = __shfl_sync(0xffffffffu, prow, k);
+      pv = __shfl_sync(0xffffffffu, pv, k);
+      if (pv < tiny || m == 0.0) {
+        broke = true;
+        break;
+      }
+      // row swap (every column, right-hand sides included: the permuted delta)
+#pragma unroll
+      for (int r = k + 1; r < P; ++r)
+        if (r == prow) {
+          const double t = col[k];
+          col[k] = col[r];
+          col[r] = t;
+        }
+      inv[k] = __ddiv_rn(1.0, __shfl_sync(0xffffffffu, col[k], k));
+      // elimination: f = lu[r][k] * inv; lu[r][c] -= f * lu[k][c] for c > k and
+      // every right-hand side (the forward substitution, same order in k)
+#pragma unroll
+      for (int r = k + 1; r < P; ++r) {
+        const double f = __dmul_rn(__shfl_sync(0xffffffffu, col[r], k), inv[k]);
+        if (lane > k) col[r] = __dsub_rn(col[r], __dmul_rn(f, col[k]));
+      }
+    }
+    if (broke) {
+      if (lane == 0) atomicMin(bad_s, blk);
+      continue;
+    }
+    // backward substitution (kernels.hpp:216-223): right-hand-side lanes
+#pragma unroll
+    for (int r = P - 1; r >= 0; --r) {
+      double accv = col[r];
+#pragma unroll
+      for (int j = r + 1; j < P; ++j) {
+        const double u = __shfl_sync(0xffffffffu, col[r], j);  // lu[r][j], column j's lane
+        if (isb) accv = __dsub_rn(accv, __dmul_rn(u, col[j]));
+      }
+      if (isb) col[r] = __dmul_rn(accv, inv[r]);
+    }
+    if (isb) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) out[(size_t)blk * P * P + r * P + cidx] = col[r];
+    }
+  }
+  __syncthreads();
+  const int bad = *bad_s;
+  __syncthreads();
+  return bad == INT_MAX ? -1 : bad;
+}
+
+// The fused fast kernels' solves: one warp per block for the tabulated block
+// widths (same results as cta_bsolve: same operations per element), else the
+// CTA-wide solver.  ws: bsolve_ws_doubles(p, blockDim.x) doubles of shared memory.
+template <int P>
+__device__ int fast_bsolve(int nblk, int p_rt, const double* gamma, const double* delta,
+                           double* out, double* ws) {
+  int* flag = reinterpret_cast<int*>(ws);
+  if constexpr (P >= 1 && P <= 16) {
+    return warp_bsolve<P>(nblk, gamma, delta, out, flag);
+  } else {
+    switch (P > 0 ? P : p_rt) {
+      case 1: return warp_bsolve<1>(nblk, gamma, delta, out, flag);
+      case 2: return warp_bsolve<2>(nblk, gamma, delta, out, flag);
+      case 4: return warp_bsolve<4>(nblk, gamma, delta, out, flag);
+      case 8: return warp_bsolve<8>(nblk, gamma, delta, out, flag);
+      case 16: return warp_bsolve<16>(nblk, gamma, delta, out, flag);
+      default: return cta_bsolve<P>(nblk, p_rt, gamma, delta, out, ws);
+    }
+  }
+}
+
 // Standalone BSOLVE launch (one CTA).  status[0] = failing block or -1.
 template <int P>
 __global__ void k_bsolve(int nblk, int p, const double* gamma, const double* delta, double* out,

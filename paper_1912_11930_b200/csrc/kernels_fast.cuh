@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k1_spmm_gram
     for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  const int bad = fast_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, (min_blocks<P, CPT>())) k2_update_gr
     for (int c = threadIdx.x; c < K; c += kThreads) a.red2[S::CS + c] = norms[c];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
+  const int bad = fast_bsolve<P>(S::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
   if (threadIdx.x == 0) a.ctrl->xpending = 1;  // K3 still owes X += P lambda
   if (bad >= 0) {
     record_breakdown(a.ctrl, bad, 2);

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kG2Threads, 2)
       a.red1[i] = (a.dist_acc ? a.red1[i] : 0.0) + alpha[i];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  const int bad = fast_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_wide(IterArgs a) {
     for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  const int bad = fast_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1W_MINB) k1_line(IterArgs a) {
     for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  const int bad = fast_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, (mma_minb<P, 2>())) k2_mma(IterArgs 
     for (int c = threadIdx.x; c < K; c += kThreads) a.red2[S::CS + c] = norms[c];
     return;
   }
-  const int bad = cta_bsolve<P>(L::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
+  const int bad = fast_bsolve<P>(L::NB, P, a.coef + S::CS, rho, beta_s, ws);  // beta
   if (threadIdx.x == 0) a.ctrl->xpending = 1;
   if (bad >= 0) {
     record_breakdown(a.ctrl, bad, 2);
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, BKG_K1_MINB) k1_tile(IterArgs a) {
     for (int i = threadIdx.x; i < S::CS; i += kThreads) a.red1[i] = alpha[i];
     return;
   }
-  const int bad = cta_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
+  const int bad = fast_bsolve<P>(S::NB, P, alpha, a.coef + S::CS, a.coef, ws);  // lambda
   if (bad >= 0) record_breakdown(a.ctrl, bad, 1);
 }
 

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int c = threadIdx.x; c < K; c += kThreads) norms[c] = sqrt(norms[c]);
   __syncthreads();
-  const int bad = cta_bsolve<P>(S::NB, P, a.coef + S::CS, rho_s, beta_s, ws);  // beta
+  const int bad = fast_bsolve<P>(S::NB, P, a.coef + S::CS, rho_s, beta_s, ws);  // beta
   if (threadIdx.x == 0) a.ctrl->xpending = 1;
   if (bad >= 0) {
     record_breakdown(a.ctrl, bad, 2);

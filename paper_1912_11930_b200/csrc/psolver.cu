@@ -87,7 +87,7 @@ __global__ void k_dist_lambda(Ctrl* ctrl, int nblk, int p, const double* red1, d
   if (stopped(ctrl)) return;
   extern __shared__ double ws[];
   for (int i = threadIdx.x; i < cs; i += blockDim.x) coef[cs + i] = red1[cs + i];
-  const int bad = cta_bsolve<0>(nblk, p, red1, red1 + cs, coef, ws);
+  const int bad = fast_bsolve<0>(nblk, p, red1, red1 + cs, coef, ws);
   if (bad >= 0) record_breakdown(ctrl, bad, 1);
 }
 
@@ -97,7 +97,7 @@ __global__ void k_dist_beta(Ctrl* ctrl, int nblk, int p, int k, const double* re
   if (stopped(ctrl)) return;
   extern __shared__ double ws[];
   double* norms = ws + bsolve_ws_doubles(p, blockDim.x);
-  const int bad = cta_bsolve<0>(nblk, p, coef + cs, red2, coef + 2 * cs, ws);
+  const int bad = fast_bsolve<0>(nblk, p, coef + cs, red2, coef + 2 * cs, ws);
   if (threadIdx.x == 0) ctrl->xpending = 1;
   if (bad >= 0) {
     record_breakdown(ctrl, bad, 2);
