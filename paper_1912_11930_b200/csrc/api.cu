@@ -1437,9 +1437,29 @@ struct bkg_solver {
     cudaEventDestroy(e1);
   }
 
+  // Q = A X through the solve's own K1 when that is one of the grid kernels
+  // (k1_grid / k1_grid2: ~3 ms on C5 where the standalone CSR SpMM takes tens of
+  // ms): same launch with P := X, its Gram / lambda by-products sent to a
+  // scratch coefficient block and a scratch control block.
+  DevBuf<double> spmm_coef;
+  DevBuf<char> spmm_ctrl;
+  bool spmm_by_k1(const double* x) {
+    if (!fast || k1_kind != 4) return false;
+    spmm_coef.ensure((size_t)6 * cs);
+    spmm_ctrl.ensure(sizeof(Ctrl));
+    BKG_CUDA_CHECK(cudaMemsetAsync(spmm_coef.ptr, 0, spmm_coef.bytes(), ctx->stream));
+    BKG_CUDA_CHECK(cudaMemsetAsync(spmm_ctrl.ptr, 0, sizeof(Ctrl), ctx->stream));
+    IterArgs a = iter_args(false);
+    a.P = const_cast<double*>(x);
+    a.coef = spmm_coef.ptr;
+    a.ctrl = reinterpret_cast<Ctrl*>(spmm_ctrl.ptr);
+    launch_k1(a);
+    return true;
+  }
+
   void final_residual(double* final_norms_host) {  // solver.hpp:203-207
     const int64_t nk = n * (int64_t)k;
-    dev_spmm(ctx, A, k, X.ptr, Q.ptr, nullptr, !fast);
+    if (!spmm_by_k1(X.ptr)) dev_spmm(ctx, A, k, X.ptr, Q.ptr, nullptr, !fast);
     const double* b = B.ptr;
     double* q = Q.ptr;
     int64_t tot = nk;

@@ -170,10 +170,11 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
   if (hbad) {
     // not one value per offset: variable coefficients on a 5 / 7-point star?
     // (whole matrices; TMA strides need an even nx)
-    // BKG_GRID_VAR=0/1 forces it off/on; default: 2-D grids only (k1_grid2:
-    // C3 K1 0.313 -> 0.215 ms; the 3-D variant is unmeasured at scale).
+    // BKG_GRID_VAR=0 turns it off.  B200: C3 (2-D) K1 0.313 -> 0.215 ms; 3-D
+    // D A D of the 7-point stencil, 128^3 k = 32: 0.351 -> 0.244 ms, 160^3 k = 64:
+    // 1.82 -> 0.86 ms (tools/var3d_probe.py).
     const char* ev = std::getenv("BKG_GRID_VAR");
-    const bool want = ev ? ev[0] == '1' : nzg == 1;
+    const bool want = !(ev && ev[0] == '0');
     if (r0 != 0 || nglobal != n || (nx & 1) || !want) return;
     st.dia.alloc((size_t)7 * n);
     BKG_CUDA_CHECK(cudaMemsetAsync(st.dia.ptr, 0, st.dia.bytes(), c->stream));

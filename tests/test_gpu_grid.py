@@ -82,9 +82,8 @@ def test_grid_first_step_ring_depths(port, grid_on, monkeypatch, ns):
 def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
     """Variable coefficients on a 5 / 7-point star run k1_grid from the DIA
     tiles (2-D heterogeneous Poisson, the C3 lognormal field, a 7-point stencil
-    with one value changed or one entry pair removed; opt-in BKG_GRID_VAR=1); an
-    odd nx (TMA stride), the default and irregular patterns keep the CSR kernels.
-    All correct."""
+    with one value changed or one entry pair removed); an odd nx (TMA stride),
+    BKG_GRID_VAR=0 and irregular patterns keep the CSR kernels.  All correct."""
     monkeypatch.setenv("BKG_GRID_VAR", "1")
     for kind, dims in [(1, (32, 32, 1)), (2, (32, 24, 1)), (2, (70, 33, 1))]:
         a = bk.stencil(kind, *dims, seed=11)
@@ -114,12 +113,13 @@ def test_grid_variable_coefficients_and_rejects(port, grid_on, monkeypatch):
     cnt[col] -= 1
     rp3 = np.concatenate([[0], np.cumsum(cnt)]).astype(np.uint64)
     _first_step(port, (rp3, ci[keep], v[keep]), n, 16, 4, False, True)
-    monkeypatch.delenv("BKG_GRID_VAR")  # default: variable coefficients on 2-D grids only
-    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
+    monkeypatch.delenv("BKG_GRID_VAR")  # on by default, 2-D and 3-D
+    _first_step(port, (rp, ci, v2), n, 16, 4, False, True)
     a2 = bk.stencil(2, 32, 24, 1, seed=11)
     _first_step(port, _csr(a2), a2.n(), 16, 4, False, True)
     monkeypatch.setenv("BKG_GRID_VAR", "0")
     _first_step(port, _csr(a2), a2.n(), 16, 4, False, False)
+    _first_step(port, (rp, ci, v2), n, 16, 4, False, False)
     monkeypatch.delenv("BKG_GRID_VAR")
     # a small 27-point grid is accepted (constant path)
     a4 = bk.stencil(4, 9, 8, 7, seed=11)
