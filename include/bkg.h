@@ -150,8 +150,9 @@ int bkg_solve_history(bkg_ctx* ctx, double* history, uint64_t cap, uint64_t* row
 /* Which K1 (SpMM + alpha Gram) the context's last bkg_solve ran: -1 exact /
  * unfused kernels, 0 k1_wide (sliced ELL), 1 k1_line (line-window sliced
  * ELL), 2 k1_stage (TMA-staged row blocks), 3 the whole loop in the
- * persistent cooperative kernel for small systems (k_resident).  Tests assert
- * the headline configs run the kernel the bench measures.                   */
+ * persistent cooperative kernel for small systems (k_resident), 4 k1_grid /
+ * k1_grid2 (grid stencils from TMA-tiled operand planes / lines).  Tests
+ * assert the headline configs run the kernel the bench measures.            */
 int bkg_solve_k1_variant(bkg_ctx* ctx, int* variant);
 
 /* ---- device-resident solver (bench / repeated solves) ------------------- */

@@ -1147,9 +1147,10 @@ struct bkg_solver {
     a.Pold = nullptr;
     if (fast && k1_kind == 2) {
       stage_args(a, A->stage, stage_ns);
-    } else if (fast && ft.sell_rows) {
+    } else if (fast && ft.sell_rows && k1_kind != 4) {
       // sliced-ELL copy for K1, built once per matrix (never inside a graph
-      // capture: launch_chunk calls iter_args before capturing)
+      // capture: launch_chunk calls iter_args before capturing); the grid
+      // kernels read no copy of the matrix
       if (A->sell.rows != ft.sell_rows || A->sell.n != n || A->sell.run != k1_run)
         sell_build(ctx, n, A->rowptr.ptr, A->cols.ptr, A->vals.ptr, ft.sell_rows, A->sell,
                    &ctx->spare_sell, k1_run);
