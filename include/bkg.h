@@ -192,6 +192,16 @@ typedef struct bkg_psolver bkg_psolver;
  * (dst, src, first row, rows) into out (4 int64 each, up to cap).          */
 int bkg_halo_plan(int nparts, const int64_t* row_begin, const int64_t* need_lo,
                   const int64_t* need_hi, int64_t* out, uint64_t cap, uint64_t* count);
+/* Work plan of the grid-stencil K1 (k1_grid / k1_grid2) for an
+ * nx x ny x nz grid (nz = 1: 2-D), k right-hand sides, sm_count SMs: pure host
+ * logic, no device needed.  Rows produced are planes (2-D: lines) [zbeg, zend)
+ * of a part whose plane 0 is plane zoff of an operand tensor of nzt planes
+ * (one solver: 0, nz, 0, nz).  out (12 values): tiles_x, tiles_y, planes per
+ * item, items per (tile, slice), slices, items, CTAs, first / last existing
+ * tensor plane in part coordinates, plane stride between items, pacing segment
+ * (0: off), pacing lead.                                                    */
+int bkg_grid_plan(int64_t nx, int64_t ny, int64_t nz, uint64_t k, int sm_count, int zbeg, int zend,
+                  int zoff, int nzt, int64_t* out);
 /* NCCL unique id (128 bytes) for bkg_psolver_create_nccl, made on rank 0.  */
 int bkg_nccl_unique_id(void* id_out);
 /* All parts on this context's device (single-GPU emulation of nparts ranks;

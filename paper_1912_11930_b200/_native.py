@@ -109,6 +109,8 @@ SIGNATURES = [
     ("bkg_solver_profile", C.c_int, [_vp, C.c_uint64, _d]),
     ("bkg_solver_debug_first_step", C.c_int, [_vp, _d, _d]),
     ("bkg_solver_kernel_bytes", C.c_int, [_vp, _d]),
+    ("bkg_grid_plan", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_int,
+                                C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
     ("bkg_halo_plan", C.c_int, [C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_uint64, _u]),
     ("bkg_nccl_unique_id", C.c_int, [C.c_void_p]),

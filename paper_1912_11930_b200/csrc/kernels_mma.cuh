@@ -156,6 +156,12 @@ __device__ __forceinline__ void mma_prefetch_block(const double* base, int64_t r
                  : "memory");
 }
 
+// Tuning: the P = 16 skip launch (XM 1: P, R in, P' out -- K2's byte mix) at
+// K2's shape, one row block per step and 3 CTAs per SM, instead of two row
+// blocks at 2 CTAs per SM.
+#ifndef BKG_K3_SKIP3
+#define BKG_K3_SKIP3 0
+#endif
 template <int P, int KERNEL>
 constexpr int mma_minb() {
   return P <= 8 ? (KERNEL == 2 ? BKG_K2_MINB8 : BKG_K3_MINB8) : (KERNEL == 2 ? 3 : 2);
@@ -318,7 +324,7 @@ __device__ __forceinline__ void k3_mma_body(const IterArgs& a) {
   double* Pout = XM == 0 ? a.P : a.Pn;
   // U row blocks per warp step, all loads issued before any DMMA: the skip
   // launch (XM 1) streams only P and R, too few bytes in flight at one block
-  constexpr int U = (XM == 1 && (P <= 8 || K == 64)) ? 2 : 1;  // C4 p = 16: slower
+  constexpr int U = (XM == 1 && (P <= 8 || K == 64) && !(BKG_K3_SKIP3 && P > 8)) ? 2 : 1;  // C4 p = 16: slower
   for (int64_t rb0 = ((int64_t)blockIdx.x * (kThreads / 32) + warp) / L::Q; rb0 < nrb;
        rb0 += U * wstride) {
     double pa[U][L::KC], po[U][L::KC], xc[U][L::NT][2], pn[U][L::NT][2], zz[U][L::NT][2];
@@ -437,7 +443,8 @@ __device__ __forceinline__ void k3_mma_body(const IterArgs& a) {
   }
 }
 template <int K, int P, bool GLOBAL, bool JAC = false, bool ZS = false, int XM = 0>
-__global__ void __launch_bounds__(kThreads, (mma_minb<P, 3>())) k3_mma(IterArgs a) {
+__global__ void __launch_bounds__(kThreads, (BKG_K3_SKIP3 && XM == 1 && P > 8 ? 3 : mma_minb<P, 3>()))
+    k3_mma(IterArgs a) {
   k3_mma_body<K, P, GLOBAL, JAC, ZS, XM>(a);
 }
 

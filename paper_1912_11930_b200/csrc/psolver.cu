@@ -801,6 +801,28 @@ int bkg_halo_plan(int nparts, const int64_t* row_begin, const int64_t* need_lo,
   });
 }
 
+int bkg_grid_plan(int64_t nx, int64_t ny, int64_t nz, uint64_t k, int sm_count, int zbeg, int zend,
+                  int zoff, int nzt, int64_t* out) {
+  return pguard([&] {
+    BKG_REQUIRE(nx > 0 && ny > 0 && nz > 0 && k > 0 && k % kGridW == 0 && sm_count > 0 &&
+                    zbeg >= 0 && zend > zbeg && zend <= nz,
+                BKG_CONFIG, "grid plan: bad shape");
+    GridStencil st;
+    st.nx = (int)nx;
+    st.ny = (int)ny;
+    st.nz = (int)nz;
+    GridArgs g{};
+    int ctas = 0;
+    if (nz == 1)
+      grid2_plan(st, (int)k, sm_count, 3, &g, &ctas);
+    else
+      grid_plan(st, (int)k, sm_count, 3, zbeg, zend, zoff, nzt, &g, &ctas);
+    const int64_t v[12] = {g.tx, g.ty, g.zchunk, g.nzc, (int64_t)(k / kGridW), g.nitems, ctas,
+                           g.tmin, g.tmax, g.zstride, g.sync_every, g.sync_lead};
+    for (int i = 0; i < 12; ++i) out[i] = v[i];
+  });
+}
+
 int bkg_nccl_unique_id(void* id_out) {
   return pguard([&] {
     ncclUniqueId id;
