@@ -731,7 +731,7 @@ bool bkg::use_grid(bkg_ctx* c, const bkg_matrix* A, const FastTable& ft, int K, 
   if (ns < 2) return false;
   grid_plan(st, K, c->sm_count, ns, 0, st.nz, 0, st.nz, g, ctas);
   *smem = ft.grid_smem(ns, st.var);
-  for (int v = 0; v < 6; ++v) allow_smem(ft.k1_grid[v], *smem);
+  for (int v = 0; v < 8; ++v) allow_smem(ft.k1_grid[v], *smem);
   return true;
 }
 
@@ -1051,7 +1051,9 @@ struct bkg_solver {
       else
         ft.k1 = A->gridst.var
                     ? ft.k1_grid[4 + (grid_args.sync_every > 0 ? 1 : 0)]
-                    : ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
+                    : A->gridst.iso27
+                          ? ft.k1_grid[6 + (grid_args.sync_every > 0 ? 1 : 0)]
+                          : ft.k1_grid[(A->gridst.full27 ? 1 : 0) + (grid_args.sync_every > 0 ? 2 : 0)];
       ft.smem_k1 = smem;
       k1_threads = grid_2d ? kG2Threads : kGridThreads;
       grid_maps.clear();

@@ -201,6 +201,7 @@ struct GridStencil {
   int nx = 0, ny = 0, nz = 0;  // nz: planes of these rows (a z-slab part: its own)
   int zs = 0, nzg = 0;         // first global plane of the rows, planes of the global grid
   bool full27 = false;  // entries off the 7-point star
+  bool iso27 = false;   // 27-point, one coefficient each for centre / faces / edges / corners
   double c[3][9] = {};
   // Variable coefficients (ok stays false): the pattern is a 5 / 7-point star
   // on the grid and dia holds its DIA copy V[slot * n + row], slots dz-1 |

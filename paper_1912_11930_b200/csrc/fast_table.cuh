@@ -94,7 +94,8 @@ struct FastTable {
   // planes, kernels_grid.cuh): [0] 7-point, [1] 27-point; [+2] with the
   // lockstep pacing compiled in (long launches); [4], [5]: 5 / 7-point with
   // variable coefficients (DIA tiles), unpaced / paced
-  const void* k1_grid[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // [6], [7]: isotropic 27-point (class sums), unpaced / paced
+  const void* k1_grid[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool grid_auto = false;  // the solver may pick it without BKG_K1_GRID=1
   int (*grid_smem)(int ns, bool var) = nullptr;
   // 2-D grids (kernels_grid2.cuh): [0] 5-point, [1] 9-point, [2] 5-point variable
@@ -152,6 +153,8 @@ void fill_table(FastTable* t) {
       t->k1_grid[3] = (const void*)&k1_grid<K, P, G, true, true>;
       t->k1_grid[4] = (const void*)&k1_grid<K, P, G, false, false, true>;
       t->k1_grid[5] = (const void*)&k1_grid<K, P, G, false, true, true>;
+      t->k1_grid[6] = (const void*)&k1_grid<K, P, G, true, false, false, true>;
+      t->k1_grid[7] = (const void*)&k1_grid<K, P, G, true, true, false, true>;
       t->k1_grid2[0] = (const void*)&k1_grid2<K, P, G, false, false>;
       t->k1_grid2[1] = (const void*)&k1_grid2<K, P, G, true, false>;
       t->k1_grid2[2] = (const void*)&k1_grid2<K, P, G, false, true>;

@@ -199,6 +199,16 @@ void grid_stencil_rows(bkg_ctx* c, int64_t n, const int64_t* rowptr, const int32
     const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
     if (cf.c[o] != 0.0 && (dx != 0) + (dy != 0) + (dz != 0) > 1) st.full27 = true;
   }
+  // isotropic: the coefficient depends only on the number of nonzero offsets
+  st.iso27 = st.full27;
+  for (int o = 0; o < 27 && st.iso27; ++o) {
+    const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+    const int cls = (dx != 0) + (dy != 0) + (dz != 0);
+    const double want = cls == 0 ? cf.c[13] : cls == 1 ? cf.c[12] : cls == 2 ? cf.c[9] : cf.c[0];
+    if (cf.c[o] != want) st.iso27 = false;
+  }
+  const char* ei = std::getenv("BKG_GRID_ISO");
+  if (ei && ei[0] == '0') st.iso27 = false;
 }
 
 // A->gridst, cached per matrix.

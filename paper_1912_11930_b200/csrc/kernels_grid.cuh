@@ -147,10 +147,11 @@ __device__ void gather_gram_grid(const double* red, double* blocks) {
 
 // PACE: the lockstep pacing compiled in (GridArgs::sync_every > 0 launches;
 // its live state costs the 27-point loop 14% when merely present).
-template <int K, int P, bool GLOBAL, bool FULL27, bool PACE, bool VAR = false>
+template <int K, int P, bool GLOBAL, bool FULL27, bool PACE, bool VAR = false, bool ISO = false>
 __global__ void __launch_bounds__(kGridThreads, 1)
     k1_grid(IterArgs a, GridArgs g, const __grid_constant__ GridMaps tm) {
   static_assert(!(VAR && FULL27), "variable coefficients: 5 / 7-point stencils");
+  static_assert(!ISO || (FULL27 && BKG_GRID_ARR == 1), "isotropic form: 27-point, 8 x 2 groups");
   constexpr int STAGE = VAR ? kGridStageBytesVar : kGridStageBytes;
   using S = FastSmem<K, P, 1, GLOBAL>;
   constexpr int NSL = K / kGridW;
@@ -306,51 +307,106 @@ __global__ void __launch_bounds__(kGridThreads, 1)
           na[q][1] = acc_b[q][1];
           nb[q][0] = nb[q][1] = 0.0;
         }
+        if constexpr (ISO) {
+          // Isotropic 27-point stencil: a coefficient depends only on how many
+          // of dx, dy, dz are nonzero (centre c0, faces cf, edges ce, corners cc).
+          // Per point and plane three sums -- the centre value, its 4 in-plane
+          // face neighbours, its 4 in-plane diagonal neighbours -- feed row t
+          // (c0, cf, ce) and rows t-1 / t+1 (cf, ce, cc, the same number w):
+          // 15 FP64 operations per point and column instead of 27 FMAs.  The
+          // two groups of a window row pair are done together (12 reads each).
+          const double c0 = g.c[1][4], cf = g.c[1][1], ce = g.c[1][0], cc = g.c[0][0];
 #pragma unroll
-        for (int py = 0; py < kGridWinY; ++py)
+          for (int yo = 0; yo < 2; ++yo) {
+            double s0[2][2], s1[2][2], s2[2][2];
 #pragma unroll
-          for (int px = 0; px < kGridWinX; ++px) {
-            bool any = false;
+            for (int xo = 0; xo < 2; ++xo)
+              s0[xo][0] = s0[xo][1] = s1[xo][0] = s1[xo][1] = s2[xo][0] = s2[xo][1] = 0.0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
-              if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && (FULL27 || dx == 0 || dy == 0))
-                any = true;
-            }
-            if (!any) continue;
-            const int row = ri0 + (py - 1) * kGridPitch + (px - 1);
-            const double2 v =
-                *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
+            for (int wy = 0; wy < 3; ++wy)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
-              if (dx < -1 || dx > 1 || dy < -1 || dy > 1) continue;
-              if (!(FULL27 || dx == 0 || dy == 0)) continue;
-              const int o = (dy + 1) * 3 + dx + 1;
-              double c0 = g.c[1][o], cp = g.c[2][o], cm = g.c[0][o];
-              if constexpr (VAR) {  // row q's own coefficients from the DIA tiles
-                const int pq = grid_gy(q) * kGridBX + grid_gx(q);
-                const int sl = o == 1 ? 0 : o == 3 ? 1 : o == 4 ? 2 : o == 5 ? 3 : 4;
-                c0 = sv[sl * kGridTile + pq];
-                if (o == 4) {
-                  cp = sv[5 * kGridTile + pq];
-                  cm = sv[6 * kGridTile + pq];
+              for (int px = 0; px < 4; ++px) {
+                const int row = ri0 + (yo + wy - 1) * kGridPitch + (px - 1);
+                const double2 v =
+                    *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
+#pragma unroll
+                for (int xo = 0; xo < 2; ++xo) {
+                  const int dx = px - 1 - xo;
+                  if (dx < -1 || dx > 1) continue;
+                  const int cls = (dx != 0) + (wy != 1);
+                  if (cls == 0) {
+                    s0[xo][0] = v.x;
+                    s0[xo][1] = v.y;
+                  } else if (cls == 1) {
+                    s1[xo][0] += v.x;
+                    s1[xo][1] += v.y;
+                  } else {
+                    s2[xo][0] += v.x;
+                    s2[xo][1] += v.y;
+                  }
                 }
               }
-              na[q][0] = fma(c0, v.x, na[q][0]);
-              na[q][1] = fma(c0, v.y, na[q][1]);
-              if (FULL27 || o == 4) {
-                qa[q][0] = fma(cp, v.x, qa[q][0]);
-                qa[q][1] = fma(cp, v.y, qa[q][1]);
-                nb[q][0] = fma(cm, v.x, nb[q][0]);
-                nb[q][1] = fma(cm, v.y, nb[q][1]);
-              }
-              if (o == 4) {  // the group's own point: next step's Gram operand
-                acc_b[q][0] = v.x;  // parked in acc_b (dead: copied into na above)
-                acc_b[q][1] = v.y;
+#pragma unroll
+            for (int xo = 0; xo < 2; ++xo) {
+              const int q = yo * 2 + xo;
+#pragma unroll
+              for (int cidx = 0; cidx < 2; ++cidx) {
+                const double w = fma(cc, s2[xo][cidx], fma(ce, s1[xo][cidx], cf * s0[xo][cidx]));
+                na[q][cidx] =
+                    fma(ce, s2[xo][cidx], fma(cf, s1[xo][cidx], fma(c0, s0[xo][cidx], na[q][cidx])));
+                qa[q][cidx] += w;
+                nb[q][cidx] = w;
+                acc_b[q][cidx] = s0[xo][cidx];  // parked: next step's Gram operand
               }
             }
           }
+        } else {
+  #pragma unroll
+          for (int py = 0; py < kGridWinY; ++py)
+  #pragma unroll
+            for (int px = 0; px < kGridWinX; ++px) {
+              bool any = false;
+  #pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
+                if (dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && (FULL27 || dx == 0 || dy == 0))
+                  any = true;
+              }
+              if (!any) continue;
+              const int row = ri0 + (py - 1) * kGridPitch + (px - 1);
+              const double2 v =
+                  *reinterpret_cast<const double2*>(st + row * 128 + ((m ^ (row & 7)) << 4));
+  #pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int dx = px - 1 - grid_gx(q), dy = py - 1 - grid_gy(q);
+                if (dx < -1 || dx > 1 || dy < -1 || dy > 1) continue;
+                if (!(FULL27 || dx == 0 || dy == 0)) continue;
+                const int o = (dy + 1) * 3 + dx + 1;
+                double c0 = g.c[1][o], cp = g.c[2][o], cm = g.c[0][o];
+                if constexpr (VAR) {  // row q's own coefficients from the DIA tiles
+                  const int pq = grid_gy(q) * kGridBX + grid_gx(q);
+                  const int sl = o == 1 ? 0 : o == 3 ? 1 : o == 4 ? 2 : o == 5 ? 3 : 4;
+                  c0 = sv[sl * kGridTile + pq];
+                  if (o == 4) {
+                    cp = sv[5 * kGridTile + pq];
+                    cm = sv[6 * kGridTile + pq];
+                  }
+                }
+                na[q][0] = fma(c0, v.x, na[q][0]);
+                na[q][1] = fma(c0, v.y, na[q][1]);
+                if (FULL27 || o == 4) {
+                  qa[q][0] = fma(cp, v.x, qa[q][0]);
+                  qa[q][1] = fma(cp, v.y, qa[q][1]);
+                  nb[q][0] = fma(cm, v.x, nb[q][0]);
+                  nb[q][1] = fma(cm, v.y, nb[q][1]);
+                }
+                if (o == 4) {  // the group's own point: next step's Gram operand
+                  acc_b[q][0] = v.x;  // parked in acc_b (dead: copied into na above)
+                  acc_b[q][1] = v.y;
+                }
+              }
+            }
+        }
         if (emit) emit_rows(t, qa);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {

@@ -344,7 +344,7 @@ struct bkg_psolver {
     pt.k1_kind = 4;
     pt.k1 = ft.k1_grid[st.full27 ? 1 : 0];  // + 2: paced (interior launch, chosen per launch)
     pt.smem_k1 = ft.grid_smem(ns, false);
-    for (int v = 0; v < 4; ++v) allow_smem(ft.k1_grid[v], pt.smem_k1);
+    for (int v = 0; v < 8; ++v) allow_smem(ft.k1_grid[v], pt.smem_k1);
     const int zoff = lower ? 1 : 0;
     const int zb = lower ? 1 : 0, ze = upper ? st.nz - 1 : st.nz;
     const char* hs = std::getenv("BKG_HALO_SMS");
@@ -574,7 +574,9 @@ struct bkg_psolver {
       GridArgs ga = interior ? pt.ga_in : pt.ga_bd;
       const int cur = a.P == pt.P[1] ? 1 : 0;
       void* gargs[] = {&a, &ga, pt.tmap[cur].bytes};
-      const void* fn = ft.k1_grid[(pt.gst.full27 ? 1 : 0) + (ga.sync_every > 0 ? 2 : 0)];
+      const void* fn = pt.gst.iso27
+                           ? ft.k1_grid[6 + (ga.sync_every > 0 ? 1 : 0)]
+                           : ft.k1_grid[(pt.gst.full27 ? 1 : 0) + (ga.sync_every > 0 ? 2 : 0)];
       launch(ctx, fn, interior ? pt.g1i : pt.g1b, kGridThreads, pt.smem_k1, gargs);
       return;
     }
