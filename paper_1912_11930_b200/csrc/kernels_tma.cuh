@@ -30,6 +30,11 @@
 //
 // Rare launches (the solve stops in this K3, a lambda breakdown flush) take
 // the register-operand kernel's body instead (k3_mma_body).
+//
+// Measured on B200: parity green, but level with the
+// register-operand kernels (C5 K2 4.52 vs 4.47 ms, K3 7.09 vs 7.16) -- at p = 16
+// the DMMA work, not the access pattern, is what keeps K2 / K3 below the
+// roofline -- so the solver takes these only with BKG_TMA23=1.
 #pragma once
 
 #include <cuda.h>
